@@ -1,0 +1,339 @@
+// K3: block-probe column mass (K3a) and shared-budget KV selection (K3b).
+//
+// K3a is the (N/B)^2 d probe of block_probe.py:44-64 in float64 — at 64K
+// tokens that is 28 heads x 256 x 256 pooled scores, latency-bound (µs), not a
+// roofline kernel. K3b is a single-CTA selection: per-group token scores,
+// length-weighted kurtosis, argmin (flattest head), top-p budget on the
+// flattest group and one top-b block table per group, written out as
+// ascending index lists (kv_select.py:49-195). Scores on the probe path are
+// constant within a probe block, so every sort/scan runs over nb blocks
+// instead of N tokens; block_size = 1 degenerates to the token-exact path.
+#include <float.h>
+#include <limits.h>
+
+#include "common.cuh"
+
+namespace omni {
+
+constexpr int kSelMaxBlocks = 8192;
+
+// ----------------------------------------------------------------------- K3a
+// Scores S[h, I, J] = pq[h, I] . pk[g, J] / sqrt(d) for J <= I (block-causal
+// tril). CTA = 16 query blocks x all visible key blocks, staged through smem in
+// tiles of 32 key blocks (rows padded by one double: conflict-free f64 reads).
+__global__ void __launch_bounds__(256) probe_scores_kernel(const double* __restrict__ pq,
+                                                           const double* __restrict__ pk, int nb, int d, int rep,
+                                                           double* __restrict__ S) {
+  extern __shared__ double sh[];
+  const int ld = d + 1;
+  double* sq = sh;            // [16][ld]
+  double* sk = sh + 16 * ld;  // [32][ld]
+  const int h = blockIdx.y, g = h / rep;
+  const int I0 = blockIdx.x * 16;
+  const double scale = 1.0 / sqrt(static_cast<double>(d));
+  for (int e = threadIdx.x; e < 16 * d; e += blockDim.x) {
+    const int i = e / d, c = e % d;
+    sq[i * ld + c] = (I0 + i < nb) ? pq[((size_t)h * nb + I0 + i) * d + c] : 0.0;
+  }
+  const int jmax = min(nb, I0 + 16);
+  const int ti = threadIdx.x / 16, tj = threadIdx.x % 16;
+  const int I = I0 + ti;
+  for (int jt = 0; jt < jmax; jt += 32) {
+    __syncthreads();
+    for (int e = threadIdx.x; e < 32 * d; e += blockDim.x) {
+      const int j = e / d, c = e % d;
+      sk[j * ld + c] = (jt + j < nb) ? pk[((size_t)g * nb + jt + j) * d + c] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int jj = tj + 16 * u, J = jt + jj;
+      if (I < nb && J <= I) {
+        double acc = 0.0;
+        for (int c = 0; c < d; ++c) acc = fma(sq[ti * ld + c], sk[jj * ld + c], acc);
+        S[((size_t)h * nb + I) * nb + J] = acc * scale;
+      }
+    }
+  }
+}
+
+// Row max and sum of exp(S - max) over the visible prefix J <= I (warp/row).
+__global__ void probe_rowstats_kernel(const double* __restrict__ S, int nb, double* __restrict__ stats) {
+  const int I = blockIdx.x, h = blockIdx.y, lane = threadIdx.x;
+  const double* row = S + ((size_t)h * nb + I) * nb;
+  double mx = -DBL_MAX;
+  for (int J = lane; J <= I; J += 32) mx = fmax(mx, row[J]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  double s = 0.0;
+  for (int J = lane; J <= I; J += 32) s += exp(row[J] - mx);
+  s = warp_sum(s);
+  if (lane == 0) {
+    stats[((size_t)h * nb + I) * 2 + 0] = mx;
+    stats[((size_t)h * nb + I) * 2 + 1] = s;
+  }
+}
+
+// mass[h, J] = sum over rows I >= J (ascending, like the reference colsum) of
+// exp(S[I, J] - max_I) / sum_I.
+__global__ void probe_colsum_kernel(const double* __restrict__ S, const double* __restrict__ stats, int nb,
+                                    double* __restrict__ mass) {
+  const int h = blockIdx.y;
+  const int J = blockIdx.x * blockDim.x + threadIdx.x;
+  if (J >= nb) return;
+  double acc = 0.0;
+  for (int I = J; I < nb; ++I) {
+    const double* st = stats + ((size_t)h * nb + I) * 2;
+    acc += exp(S[((size_t)h * nb + I) * nb + J] - st[0]) / st[1];
+  }
+  mass[(size_t)h * nb + J] = acc;
+}
+
+// ----------------------------------------------------------------------- K3b
+struct SelShared {
+  double key[kSelMaxBlocks];
+  int idx[kSelMaxBlocks];
+  int take[kSelMaxBlocks];
+  double red[32];
+  double kurt[64];
+  int flat;
+  int budget;
+  double retained, total;
+};
+
+__device__ __forceinline__ int block_len(int J, int N, int B) { return min(B, N - J * B); }
+
+__device__ double block_reduce_sum(double v, double* red) {
+  v = warp_sum(v);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (threadIdx.x < 32) {
+    t = (threadIdx.x < (blockDim.x >> 5)) ? red[threadIdx.x] : 0.0;
+    t = warp_sum(t);
+    if (threadIdx.x == 0) red[0] = t;
+  }
+  __syncthreads();
+  t = red[0];
+  __syncthreads();
+  return t;
+}
+
+// Ascending bitonic sort of (key, idx) pairs, ties broken by idx: with
+// key = -score this is the reference's lexsort((arange, -a)) order.
+__device__ void bitonic_sort(double* key, int* idx, int n_pow2) {
+  for (int k = 2; k <= n_pow2; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < n_pow2; i += blockDim.x) {
+        const int p = i ^ j;
+        if (p > i) {
+          const bool up = (i & k) == 0;
+          const double ki = key[i], kp = key[p];
+          const int ii = idx[i], ip = idx[p];
+          const bool gt = (ki > kp) || (ki == kp && ii > ip);
+          if (gt == up) {
+            key[i] = kp; key[p] = ki;
+            idx[i] = ip; idx[p] = ii;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+__global__ void __launch_bounds__(1024) select_kernel(const double* __restrict__ mass, int hq, int hkv, int N, int B,
+                                                      double p, int gran, int vision_limit, int budget_override,
+                                                      int32_t* __restrict__ selected, int32_t* __restrict__ info,
+                                                      double* __restrict__ stats, double* __restrict__ gscores) {
+  extern __shared__ __align__(16) unsigned char sel_raw[];
+  SelShared& S = *reinterpret_cast<SelShared*>(sel_raw);
+  const int nb = (N + B - 1) / B;
+  const int rep = hq / hkv;
+  int np2 = 1;
+  while (np2 < nb) np2 <<= 1;
+
+  // Phase 1: per-group per-token scores (block-constant) and kurtosis.
+  for (int g = 0; g < hkv; ++g) {
+    double part = 0.0;
+    for (int J = threadIdx.x; J < nb; J += blockDim.x) {
+      const double len = static_cast<double>(block_len(J, N, B));
+      double s = mass[(size_t)(g * rep) * nb + J] / len;
+      for (int r = 1; r < rep; ++r) s += mass[(size_t)(g * rep + r) * nb + J] / len;
+      gscores[(size_t)g * nb + J] = s;
+      part += len * s;
+    }
+    __syncthreads();
+    const double mean = block_reduce_sum(part, S.red) / static_cast<double>(N);
+    double p2 = 0.0, p4 = 0.0;
+    for (int J = threadIdx.x; J < nb; J += blockDim.x) {
+      const double len = static_cast<double>(block_len(J, N, B));
+      const double dv = gscores[(size_t)g * nb + J] - mean;
+      const double d2 = dv * dv;
+      p2 += len * d2;
+      p4 += len * d2 * d2;
+    }
+    const double m2 = block_reduce_sum(p2, S.red) / static_cast<double>(N);
+    const double m4 = block_reduce_sum(p4, S.red) / static_cast<double>(N);
+    if (threadIdx.x == 0) S.kurt[g] = (m2 == 0.0) ? 0.0 : m4 / (m2 * m2);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    int f = 0;
+    for (int g = 1; g < hkv; ++g)
+      if (S.kurt[g] < S.kurt[f]) f = g;  // argmin, ties to the lowest index
+    S.flat = f;
+  }
+  __syncthreads();
+  const int flat = S.flat;
+
+  // Phase 2: budget on the flattest group (descending cumsum over tokens,
+  // evaluated block-wise: within a block of equal values cum = C + k * s).
+  if (budget_override > 0) {
+    if (threadIdx.x == 0) { S.budget = budget_override; S.retained = 0.0; S.total = 0.0; }
+  } else {
+    for (int i = threadIdx.x; i < np2; i += blockDim.x) {
+      S.key[i] = (i < nb) ? -gscores[(size_t)flat * nb + i] : DBL_MAX;
+      S.idx[i] = (i < nb) ? i : INT_MAX;
+    }
+    __syncthreads();
+    bitonic_sort(S.key, S.idx, np2);
+    if (threadIdx.x == 0) {
+      double total = 0.0;
+      for (int i = 0; i < nb; ++i) total += static_cast<double>(block_len(S.idx[i], N, B)) * (-S.key[i]);
+      const double thr = fmin(p * total, total);
+      double C = 0.0;
+      int T = 0, b = N;
+      double ret = total;
+      for (int i = 0; i < nb; ++i) {
+        const double s = -S.key[i];
+        const int len = block_len(S.idx[i], N, B);
+        const double end = C + static_cast<double>(len) * s;
+        if (end >= thr || i == nb - 1) {
+          int k = 1;
+          if (s > 0.0) {
+            double kk = ceil((thr - C) / s);
+            k = (kk < 1.0) ? 1 : (kk > len ? len : static_cast<int>(kk));
+            while (k > 1 && C + static_cast<double>(k - 1) * s >= thr) --k;
+            while (k < len && C + static_cast<double>(k) * s < thr) ++k;
+          }
+          b = T + k;
+          ret = C + static_cast<double>(k) * s;
+          break;
+        }
+        C = end;
+        T += len;
+      }
+      S.budget = b;
+      S.retained = ret;
+      S.total = total;
+    }
+  }
+  __syncthreads();
+  int b = S.budget;
+  const int span = (vision_limit >= 0) ? vision_limit : N;
+  if (b > span) b = span;
+
+  // Phase 3: per-group top-b block table -> ascending index list.
+  for (int g = 0; g < hkv; ++g) {
+    for (int i = threadIdx.x; i < np2; i += blockDim.x) {
+      if (i < nb) {
+        const double s = gscores[(size_t)g * nb + i];
+        const double rank = (gran == OMNI_GRAN_BLOCK) ? s * static_cast<double>(block_len(i, N, B)) : s;
+        S.key[i] = -rank;
+        S.idx[i] = i;
+      } else {
+        S.key[i] = DBL_MAX;
+        S.idx[i] = INT_MAX;
+      }
+      if (i < nb) S.take[i] = 0;
+    }
+    __syncthreads();
+    bitonic_sort(S.key, S.idx, np2);
+    if (threadIdx.x == 0) {
+      int left = b;
+      for (int i = 0; i < nb && left > 0; ++i) {
+        const int J = S.idx[i];
+        const int lo = J * B;
+        const int len = max(0, min(lo + block_len(J, N, B), span) - lo);
+        const int t = min(len, left);
+        S.take[J] = t;
+        left -= t;
+      }
+      int off = 0;  // exclusive prefix over blocks in index order (reuse idx[])
+      for (int J = 0; J < nb; ++J) {
+        S.idx[J] = off;
+        off += S.take[J];
+      }
+    }
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    for (int J = warp; J < nb; J += nw) {
+      const int t = S.take[J], off = S.idx[J];
+      for (int k = lane; k < t; k += 32) selected[(size_t)g * N + off + k] = J * B + k;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    info[0] = b;
+    info[1] = flat;
+    info[2] = hkv;
+    info[3] = nb;
+    for (int g = 0; g < hkv; ++g) {
+      info[4 + g] = b;  // per-group selected counts (all equal: shared budget)
+      stats[g] = S.kurt[g];
+    }
+    stats[hkv] = S.retained;
+    stats[hkv + 1] = S.total;
+  }
+}
+
+}  // namespace omni
+
+using namespace omni;
+
+extern "C" size_t omni_probe_mass_workspace(int n_q_heads, int n_blocks) {
+  return sizeof(double) * (size_t)n_q_heads * n_blocks * (n_blocks + 2);
+}
+
+extern "C" int omni_probe_mass(const double* pooled_q, const double* pooled_k, int n_q_heads, int n_kv_heads,
+                               int n_blocks, int head_dim, double* mass, void* workspace, void* stream) {
+  OMNI_CHECK(n_kv_heads >= 1 && n_q_heads % n_kv_heads == 0, OMNI_E_SHAPE, "n_q_heads must be a multiple of n_kv_heads");
+  OMNI_CHECK(head_dim >= 1 && head_dim <= 256, OMNI_E_SHAPE, "head_dim must be in [1, 256]");
+  OMNI_CHECK(n_blocks >= 1, OMNI_E_SHAPE, "no probe blocks");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  double* S = static_cast<double*>(workspace);
+  double* st = S + (size_t)n_q_heads * n_blocks * n_blocks;
+  const size_t shm = sizeof(double) * 48 * (head_dim + 1);
+  if (shm > 48 * 1024)
+    OMNI_CUDA_TRY(cudaFuncSetAttribute(probe_scores_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
+  probe_scores_kernel<<<dim3((n_blocks + 15) / 16, n_q_heads), 256, shm, s>>>(pooled_q, pooled_k, n_blocks, head_dim,
+                                                                            n_q_heads / n_kv_heads, S);
+  probe_rowstats_kernel<<<dim3(n_blocks, n_q_heads), 32, 0, s>>>(S, n_blocks, st);
+  probe_colsum_kernel<<<dim3((n_blocks + 127) / 128, n_q_heads), 128, 0, s>>>(S, st, n_blocks, mass);
+  return omni_launch_check();
+}
+
+extern "C" int omni_select(const double* block_mass, int n_q_heads, int n_kv_heads, int seq_len, int block_size,
+                           double p, int granularity, int vision_limit, int budget_override, int32_t* selected,
+                           int32_t* info, double* stats, double* group_scores, void* stream) {
+  OMNI_CHECK(p > 0.0 && p <= 1.0, OMNI_E_PARAM, "retention p must be in (0, 1]");
+  OMNI_CHECK(block_size >= 1, OMNI_E_PARAM, "block size must be >= 1");
+  OMNI_CHECK(n_kv_heads >= 1 && n_kv_heads <= 64 && n_q_heads % n_kv_heads == 0, OMNI_E_SHAPE,
+             "need 1 <= n_kv_heads <= 64 dividing n_q_heads");
+  OMNI_CHECK(granularity == OMNI_GRAN_TOKEN || granularity == OMNI_GRAN_BLOCK, OMNI_E_PARAM, "granularity must be token or block");
+  const int nb = (seq_len + block_size - 1) / block_size;
+  OMNI_CHECK(nb >= 1 && nb <= kSelMaxBlocks, OMNI_E_PARAM, "selection supports at most 8192 probe blocks");
+  OMNI_CHECK(vision_limit != 0, OMNI_E_PARAM, "vision span is empty");
+  OMNI_CHECK(budget_override <= seq_len, OMNI_E_PARAM, "budget exceeds the sequence");
+  OMNI_CHECK(group_scores != nullptr, OMNI_E_PARAM, "group_scores buffer required");
+  const size_t shm = sizeof(SelShared);
+  OMNI_CUDA_TRY(cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
+  select_kernel<<<1, 1024, shm, static_cast<cudaStream_t>(stream)>>>(block_mass, n_q_heads, n_kv_heads, seq_len,
+                                                                      block_size, p, granularity, vision_limit,
+                                                                      budget_override, selected, info, stats,
+                                                                      group_scores);
+  return omni_launch_check();
+}

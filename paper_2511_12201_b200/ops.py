@@ -1,0 +1,217 @@
+"""Device-level operators over the C ABI (torch tensors on ``cuda``).
+
+Every function here is one (or two) ``omni_*`` calls on the current torch CUDA
+stream; outputs are allocated with the torch caching allocator and passed
+down as plain pointers. No host synchronisation happens on the prefill path:
+budget, counts and tile bounds stay on the device and grids are sized by
+upper bounds.
+
+Layouts: Q [Hq, N, d], K/V [Hkv, N, d] (bf16 for attention; bf16 or fp32 for
+selection, the reference's "fp32 validation mode"). GQA rule B: Q head h
+belongs to KV group h // (Hq // Hkv).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib
+from .errors import ParameterError, ShapeError
+
+GRAN = {"token": 0, "block": 1}
+DTYPE = {torch.bfloat16: 0, torch.float32: 1}
+TILE = 128  # attention tile rows / key tile (K_sel padding)
+
+
+def _p(t: torch.Tensor | None):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else ctypes.c_void_p(0)
+
+
+def _stream():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _dtype(t: torch.Tensor) -> int:
+    if t.dtype not in DTYPE:
+        raise ShapeError(f"unsupported dtype {t.dtype}; use bfloat16 or float32")
+    return DTYPE[t.dtype]
+
+
+def _cuda3(t: torch.Tensor, name: str) -> None:
+    if not t.is_cuda:
+        raise ShapeError(f"{name} must be a CUDA tensor")
+    if t.dim() != 3 or not t.is_contiguous():
+        raise ShapeError(f"{name} must be a contiguous [heads, tokens, dim] tensor, got {tuple(t.shape)}")
+
+
+def n_blocks(n: int, block: int) -> int:
+    return math.ceil(n / block)
+
+
+def round_up(x: int, m: int) -> int:
+    return ((x + m - 1) // m) * m
+
+
+# ----------------------------------------------------------------------- K1
+def kv_probe(K: torch.Tensor, n_vision: int, sink_index: int, block_size: int):
+    """Probe keys (k_lazy = K[sink], k_act = vision mean) and pooled keys, f64.
+    query_select.py:41-47 + block_probe.py:58."""
+    _cuda3(K, "K")
+    hkv, n, d = K.shape
+    nb = n_blocks(n, block_size)
+    f64 = dict(device=K.device, dtype=torch.float64)
+    k_lazy, k_act = torch.empty(hkv, d, **f64), torch.empty(hkv, d, **f64)
+    pooled = torch.empty(hkv, nb, d, **f64)
+    ws = torch.empty(max(1, _lib.size("omni_kv_probe_workspace", hkv, n, d, block_size)), device=K.device, dtype=torch.uint8)
+    _lib.call("omni_kv_probe", _p(K), _dtype(K), hkv, n, d, n_vision, sink_index, block_size,
+              _p(k_lazy), _p(k_act), _p(pooled), _p(ws), _stream())
+    return k_lazy, k_act, pooled
+
+
+# ----------------------------------------------------------------------- K2
+def q_score(Q: torch.Tensor, k_lazy, k_act, n_vision: int, tau: float, preserve_first_head: bool, block_size: int,
+            want_prob: bool = False, O_zero: torch.Tensor | None = None):
+    """Lazy/active flags, optional p_act, pooled queries and per-block active
+    counts. query_select.py:50-92 + block_probe.py:57."""
+    _cuda3(Q, "Q")
+    hq, n, d = Q.shape
+    hkv = k_lazy.shape[0]
+    nb = n_blocks(n, block_size)
+    active = torch.empty(hq, n, device=Q.device, dtype=torch.uint8)
+    p_act = torch.empty(hq, max(n_vision, 1), device=Q.device, dtype=torch.float64) if want_prob else None
+    pooled = torch.empty(hq, nb, d, device=Q.device, dtype=torch.float64)
+    bact = torch.empty(hq, nb, device=Q.device, dtype=torch.int32)
+    if O_zero is not None:
+        _cuda3(O_zero, "O")
+        if O_zero.dtype != torch.bfloat16 or O_zero.shape != Q.shape:
+            raise ShapeError("O must be bf16 with Q's shape")
+    _lib.call("omni_q_score", _p(Q), _dtype(Q), hq, hkv, n, d, n_vision, float(tau), int(bool(preserve_first_head)),
+              block_size, _p(k_lazy), _p(k_act), _p(active), _p(p_act), _p(pooled), _p(bact), _p(O_zero), _stream())
+    return active, p_act, pooled, bact
+
+
+def compact_rows(active: torch.Tensor, block_active: torch.Tensor, block_size: int):
+    """Ascending active row positions per head (prefill.py:106) + counts."""
+    hq, n = active.shape
+    rows = torch.empty(hq, n, device=active.device, dtype=torch.int32)
+    counts = torch.empty(hq, device=active.device, dtype=torch.int32)
+    _lib.call("omni_compact_rows", _p(active), _p(block_active), hq, n, block_size, _p(rows), _p(counts), _stream())
+    return rows, counts
+
+
+# ----------------------------------------------------------------------- K3
+def probe_mass(pooled_q: torch.Tensor, pooled_k: torch.Tensor, return_workspace: bool = False):
+    """Column mass of the block-causal pooled probe per Q head, f64 [Hq, nb].
+    block_probe.py:44-64,76."""
+    hq, nb, d = pooled_q.shape
+    hkv = pooled_k.shape[0]
+    mass = torch.empty(hq, nb, device=pooled_q.device, dtype=torch.float64)
+    ws = torch.empty(_lib.size("omni_probe_mass_workspace", hq, nb) // 8, device=pooled_q.device, dtype=torch.float64)
+    _lib.call("omni_probe_mass", _p(pooled_q), _p(pooled_k), hq, hkv, nb, d, _p(mass), _p(ws), _stream())
+    if return_workspace:
+        return mass, ws
+    return mass
+
+
+@dataclass
+class Selection:
+    """Device-resident selection (kv_select.SelectionResult + scores)."""
+
+    selected: torch.Tensor      # i32 [Hkv, N]; first `counts[g]` entries valid, ascending
+    info: torch.Tensor          # i32 [4 + Hkv] = budget, flattest, Hkv, nb, counts...
+    stats: torch.Tensor         # f64 [Hkv + 2] = kurtoses..., retained, total
+    group_scores: torch.Tensor  # f64 [Hkv, nb] per-token score of each block
+
+    @property
+    def counts(self) -> torch.Tensor:
+        return self.info[4:]
+
+
+def select(mass: torch.Tensor, n_kv_heads: int, seq_len: int, block_size: int, p: float,
+           granularity: str = "token", vision_limit: int = -1, budget_override: int = 0) -> Selection:
+    """Flattest-head budget + per-group top-b (kv_select.py:49-195)."""
+    if granularity not in GRAN:
+        raise ParameterError(f"granularity must be one of {tuple(GRAN)}")
+    hq, nb = mass.shape
+    dev = mass.device
+    selected = torch.empty(n_kv_heads, seq_len, device=dev, dtype=torch.int32)
+    info = torch.empty(4 + n_kv_heads, device=dev, dtype=torch.int32)
+    stats = torch.empty(n_kv_heads + 2, device=dev, dtype=torch.float64)
+    gs = torch.empty(n_kv_heads, nb, device=dev, dtype=torch.float64)
+    _lib.call("omni_select", _p(mass), hq, n_kv_heads, seq_len, block_size, float(p), GRAN[granularity],
+              int(vision_limit), int(budget_override), _p(selected), _p(info), _p(stats), _p(gs), _stream())
+    return Selection(selected, info, stats, gs)
+
+
+# ----------------------------------------------------------------------- K6
+def gather_rows(src: torch.Tensor, idx: torch.Tensor, counts: torch.Tensor | int, dst_rows: int,
+                pad_rows: int = 1, out: torch.Tensor | None = None) -> torch.Tensor:
+    """dst[g, r] = src[g, idx[g, r]] for r < count_g; zero rows up to the next
+    multiple of pad_rows (prefill.py:109-110, decode.py:92-107)."""
+    _cuda3(src, "src")
+    g, rows, d = src.shape
+    if out is None:
+        out = torch.empty(g, dst_rows, d, device=src.device, dtype=src.dtype)
+    cnt_t = counts if isinstance(counts, torch.Tensor) else None
+    cnt_c = 0 if cnt_t is not None else int(counts)
+    _lib.call("omni_gather_rows", _p(src), _dtype(src), g, rows, d, _p(idx), idx.shape[-1], _p(cnt_t), cnt_c,
+              _p(out), dst_rows, pad_rows, _stream())
+    return out
+
+
+# ----------------------------------------------------------------------- K4
+def sparse_attn_fwd(Q, K_sel, V_sel, V, rows, counts, selected, sel_counts, sink_index: int,
+                    O: torch.Tensor, lse: torch.Tensor | None = None):
+    """tcgen05 sparse flash-attention forward into O (lazy rows untouched)."""
+    hq, n, d = Q.shape
+    hkv, cap, _ = K_sel.shape
+    if Q.dtype != torch.bfloat16 or K_sel.dtype != torch.bfloat16 or V.dtype != torch.bfloat16:
+        raise ShapeError("sparse attention consumes bf16 Q/K/V")
+    if selected.shape[-1] != n:
+        raise ShapeError("selected must be [Hkv, N]")
+    _lib.call("omni_sparse_attn_fwd", _p(Q), _p(K_sel), _p(V_sel), _p(V), _p(rows), _p(counts), _p(selected),
+              _p(sel_counts), hq, hkv, n, d, cap, sink_index, _p(O), _p(lse), _stream())
+    return O, lse
+
+
+def sparse_attn_bwd(Q, K_sel, V_sel, O, dO, lse, rows, counts, selected, sel_counts):
+    """Backward of K4 over the compacted keys; returns (dQ, dK_sel, dV_sel,
+    dV_sink) in fp32."""
+    hq, n, d = Q.shape
+    hkv, cap, _ = K_sel.shape
+    f32 = dict(device=Q.device, dtype=torch.float32)
+    dQ = torch.empty(hq, n, d, **f32)
+    dK = torch.empty(hkv, cap, d, **f32)
+    dV = torch.empty(hkv, cap, d, **f32)
+    dVs = torch.empty(hkv, d, **f32)
+    ws = torch.empty(max(1, _lib.size("omni_sparse_attn_bwd_workspace", hq, n)), device=Q.device, dtype=torch.uint8)
+    _lib.call("omni_sparse_attn_bwd", _p(Q), _p(K_sel), _p(V_sel), _p(O), _p(dO), _p(lse), _p(rows), _p(counts),
+              _p(selected), _p(sel_counts), hq, hkv, n, d, cap, _p(dQ), _p(dK), _p(dV), _p(dVs), _p(ws), _stream())
+    return dQ, dK, dV, dVs
+
+
+# ----------------------------------------------------------------------- K7
+def decode_step(q, vision_k, vision_v, vision_len, text_k, text_v, n_text: int, answer_k, answer_v, n_answer: int,
+                k_lazy, k_act, tau: float, preserve_first_head: bool, flags_override=None, out=None, flags=None):
+    """One batched slim-cache decode step (decode.py:124-194, rule B)."""
+    b, hq, d = q.shape
+    hkv, vcap = vision_k.shape[1], vision_k.shape[2]
+    acap = answer_k.shape[2]
+    dev = q.device
+    if out is None:
+        out = torch.empty(b, hq, d, device=dev, dtype=torch.float32)
+    if flags is None:
+        flags = torch.empty(b, hq, device=dev, dtype=torch.uint8)
+    ws = torch.empty(_lib.size("omni_decode_workspace", b, hq, vcap, n_text, acap, d), device=dev, dtype=torch.uint8)
+    _lib.call("omni_decode_step", _p(q), _p(vision_k), _p(vision_v), _p(vision_len), _p(text_k), _p(text_v), n_text,
+              _p(answer_k), _p(answer_v), n_answer, _p(k_lazy), _p(k_act), b, hq, hkv, d, vcap, acap, float(tau),
+              int(bool(preserve_first_head)), _p(flags_override), _p(flags), _p(out), _p(ws), _stream())
+    return out, flags
+
+
+def device_check() -> None:
+    _lib.call("omni_device_check")

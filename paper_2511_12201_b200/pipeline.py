@@ -1,0 +1,111 @@
+"""Device-resident OmniSparse prefill: K1 -> K2 -> compaction -> K3a -> K3b ->
+gather -> K4, all on one CUDA stream with no host synchronisation.
+
+This is the composite behind ``prefill.sparse_prefill`` and the benchmark.
+It follows the glue of ``prefill.py:160-175`` (minus the always-on dense
+oracle and recall instrumentation) under GQA rule B
+(DESIGN.md): masks per Q head, probe scores summed per KV group, one budget
+from the flattest group, one top-b set per group shared by its Q heads.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+
+from . import ops
+from .errors import LayoutError, ParameterError, ShapeError
+
+
+@dataclass(frozen=True)
+class SparsityConfig:
+    """``prefill.py:38-65``: every sparsity knob, validated on construction."""
+
+    tau: float = 0.08
+    p: float = 0.82
+    block_size: int = 256
+    granularity: str = "token"
+    preserve_first_head: bool = True
+    sink_index: int = 0
+    seed: int = 0
+
+    def __post_init__(self):
+        if not 0.0 <= self.tau < 1.0:
+            raise ParameterError(f"tau must be in [0, 1), got {self.tau}")
+        if not 0.0 < self.p <= 1.0:
+            raise ParameterError(f"p must be in (0, 1], got {self.p}")
+        if self.block_size < 1:
+            raise ParameterError(f"block_size must be >= 1, got {self.block_size}")
+        if self.granularity not in ("token", "block"):
+            raise ParameterError("granularity must be one of ('token', 'block')")
+
+
+@dataclass
+class DevicePrefill:
+    """All device tensors of one prefill (outputs + every intermediate)."""
+
+    outputs: torch.Tensor       # bf16 [Hq, N, d]; lazy rows zero
+    lse: torch.Tensor           # f32 [Hq, N] softmax normaliser of active rows
+    active: torch.Tensor        # u8 [Hq, N]
+    rows: torch.Tensor          # i32 [Hq, N] compacted active rows
+    counts: torch.Tensor        # i32 [Hq]
+    selection: ops.Selection
+    k_lazy: torch.Tensor
+    k_act: torch.Tensor
+    pooled_q: torch.Tensor
+    pooled_k: torch.Tensor
+    block_mass: torch.Tensor    # f64 [Hq, nb]
+    K_sel: torch.Tensor         # bf16 [Hkv, cap, d]
+    V_sel: torch.Tensor
+    p_act: torch.Tensor | None = None
+
+
+def check_qkv(Q: torch.Tensor, K: torch.Tensor, V: torch.Tensor) -> None:
+    for name, t in (("Q", Q), ("K", K), ("V", V)):
+        if not t.is_cuda or t.dim() != 3:
+            raise ShapeError(f"{name} must be a CUDA [heads, tokens, dim] tensor")
+    if K.shape != V.shape or Q.shape[1:] != K.shape[1:]:
+        raise ShapeError(f"Q {tuple(Q.shape)} / K {tuple(K.shape)} / V {tuple(V.shape)} disagree")
+    if Q.shape[0] % K.shape[0]:
+        raise ShapeError("Q heads must be a multiple of KV heads (GQA rule B)")
+
+
+def select_device(Q: torch.Tensor, K: torch.Tensor, n_vision: int, cfg: SparsityConfig, want_prob: bool = False,
+                  O_zero: torch.Tensor | None = None):
+    """Masks + probe scores + flattest/budget/top-b (no attention)."""
+    hq, n, d = Q.shape
+    if not 1 <= n_vision <= n:
+        raise LayoutError(f"n_vision {n_vision} outside [1, {n}]")
+    if not 0 <= cfg.sink_index < n:
+        raise LayoutError(f"sink_index {cfg.sink_index} outside the prompt")
+    k_lazy, k_act, pk = ops.kv_probe(K, n_vision, cfg.sink_index, cfg.block_size)
+    active, p_act, pq, bact = ops.q_score(Q, k_lazy, k_act, n_vision, cfg.tau, cfg.preserve_first_head,
+                                          cfg.block_size, want_prob=want_prob, O_zero=O_zero)
+    rows, counts = ops.compact_rows(active, bact, cfg.block_size)
+    mass = ops.probe_mass(pq, pk)
+    sel = ops.select(mass, K.shape[0], n, cfg.block_size, cfg.p, cfg.granularity)
+    return k_lazy, k_act, pk, active, p_act, pq, rows, counts, mass, sel
+
+
+def sparse_prefill_device(Q: torch.Tensor, K: torch.Tensor, V: torch.Tensor, n_vision: int,
+                          cfg: SparsityConfig = SparsityConfig(), want_prob: bool = False,
+                          out: torch.Tensor | None = None) -> DevicePrefill:
+    """Full sparse prefill of one attention layer on the GPU.
+
+    Q [Hq, N, 128] bf16 (or fp32 for selection-only validation — attention
+    then needs bf16 copies), K/V [Hkv, N, 128]."""
+    check_qkv(Q, K, V)
+    hq, n, d = Q.shape
+    hkv = K.shape[0]
+    Qb = Q if Q.dtype == torch.bfloat16 else Q.to(torch.bfloat16)
+    Kb = K if K.dtype == torch.bfloat16 else K.to(torch.bfloat16)
+    Vb = V if V.dtype == torch.bfloat16 else V.to(torch.bfloat16)
+    O = out if out is not None else torch.empty_like(Qb)
+    k_lazy, k_act, pk, active, p_act, pq, rows, counts, mass, sel = select_device(Q, K, n_vision, cfg, want_prob, O)
+    cap = ops.round_up(n, ops.TILE)
+    K_sel = ops.gather_rows(Kb, sel.selected, sel.counts, cap, ops.TILE)
+    V_sel = ops.gather_rows(Vb, sel.selected, sel.counts, cap, ops.TILE)
+    lse = torch.empty(hq, n, device=Q.device, dtype=torch.float32)
+    ops.sparse_attn_fwd(Qb, K_sel, V_sel, Vb, rows, counts, sel.selected, sel.counts, cfg.sink_index, O, lse)
+    return DevicePrefill(O, lse, active, rows, counts, sel, k_lazy, k_act, pq, pk, mass, K_sel, V_sel, p_act)

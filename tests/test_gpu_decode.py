@@ -1,0 +1,107 @@
+"""GPU parity of cache slimming (K6) and slimmed decode (K7) vs the oracle.
+
+Flags are bit-exact (float64 classification on both sides); outputs within
+1e-3 (bf16 cache values are identical on both sides; fp32 accumulation)."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import attention as oatt
+from oracle import pipeline as opipe
+from oracle.workload import Spec, decode_inputs, generate, round_bf16
+
+pytestmark = pytest.mark.gpu
+
+
+def dev(x, dtype=torch.bfloat16):
+    return torch.tensor(np.asarray(x), dtype=dtype, device="cuda")
+
+
+def build_pair(seed, hq=8, hkv=2, nv=2000, nt=48, steps=6, tau=0.08, lazy=0.5):
+    from paper_2511_12201_b200 import decode as gdec
+    from paper_2511_12201_b200 import ops
+    from paper_2511_12201_b200.pipeline import SparsityConfig, sparse_prefill_device
+
+    spec = Spec(heads=hq, heads_kv=hkv, head_dim=128, n_vision=nv, n_text=nt, seed=seed, lazy_fraction=lazy)
+    Q, K, V = (round_bf16(x) for x in generate(spec))
+    n = nv + nt
+    res = sparse_prefill_device(dev(Q), dev(K), dev(V), nv, SparsityConfig(tau=tau))
+    b = int(res.selection.info[0])
+    vsel = ops.select(res.block_mass, hkv, n, 256, 0.82, "token", vision_limit=nv, budget_override=b)
+    bv = int(vsel.info[0])
+    cache = gdec.build_cache(dev(K), dev(V), vsel.selected, bv, nv, nt, res.k_lazy, res.k_act, hq,
+                             answer_capacity=16)
+    ref = opipe.select(Q, K, nv, 0, tau, 0.82, 256)
+    rb, rsel = opipe.vision_selection(ref, nv)
+    assert rb == bv
+    for g in range(hkv):
+        np.testing.assert_array_equal(vsel.selected[g, :bv].cpu().numpy(), rsel[g])
+    ocache = oatt.build_cache(K, V, rsel, rb, nv, nt, 0)
+    trace = decode_inputs(spec, K, steps, np.random.default_rng(100 + seed))
+    trace = [(round_bf16(q), round_bf16(k), round_bf16(v)) for q, k, v in trace]
+    return cache, ocache, trace, hq // hkv
+
+
+def test_build_cache_gathers_selected_rows():
+    cache, ocache, _, _ = build_pair(0)
+    b = cache.budgets[0]
+    for g in range(cache.n_kv_heads):
+        np.testing.assert_array_equal(cache.vision_k[0, g, :b].float().cpu().numpy(), ocache[g].vision_k)
+        np.testing.assert_array_equal(cache.vision_v[0, g, :b].float().cpu().numpy(), ocache[g].vision_v)
+        np.testing.assert_array_equal(cache.vision_indices[0, g, :b].cpu().numpy(), ocache[g].vision_indices)
+        np.testing.assert_allclose(cache.k_act[0, g].cpu().numpy(), ocache[g].k_act, rtol=1e-13)
+        np.testing.assert_array_equal(cache.k_lazy[0, g].cpu().numpy(), ocache[g].k_lazy)
+
+
+def test_decode_trace_matches_oracle():
+    from paper_2511_12201_b200 import decode as gdec
+
+    cache, ocache, trace, rep = build_pair(1)
+    log = oatt.FetchLog()
+    for q, k, v in trace:
+        out, flags = gdec.decode_attention(dev(q).unsqueeze(0), cache, 0.08)
+        o_ref, f_ref = oatt.decode_step(q, ocache, 0.08, rep, True, log)
+        np.testing.assert_array_equal(flags[0].cpu().numpy().astype(bool), f_ref)
+        np.testing.assert_allclose(out[0].cpu().numpy(), np.stack(o_ref), atol=1e-3, rtol=1e-3)
+        gdec.append_answer(cache, dev(k).unsqueeze(0), dev(v).unsqueeze(0))
+        oatt.append_answer(ocache, k, v, 128)
+    assert cache.fetch.vision_tokens == log.vision_tokens
+    assert cache.fetch.step_active_heads == log.step_active_heads
+
+
+def test_forced_flags_exclusion_semantics():
+    from paper_2511_12201_b200 import decode as gdec
+
+    cache, ocache, trace, rep = build_pair(2)
+    q = trace[0][0]
+    forced = np.zeros(cache.n_q_heads, dtype=bool)
+    forced[[0, 3, 5]] = True
+    out, fl = gdec.decode_attention(dev(q).unsqueeze(0), cache, 0.08, flags=torch.tensor(forced[None]))
+    np.testing.assert_array_equal(fl[0].cpu().numpy().astype(bool), forced)
+    exp = np.stack(oatt.decode_dense(q, ocache, forced, rep))
+    np.testing.assert_allclose(out[0].cpu().numpy(), exp, atol=1e-3, rtol=1e-3)
+
+
+def test_batched_decode_ragged_budgets():
+    """Batch of sequences with different budgets and lazy patterns (C5 shape
+    logic at small N): every sequence matches its own oracle."""
+    from paper_2511_12201_b200 import decode as gdec
+
+    pairs = [build_pair(s, lazy=0.3 + 0.2 * s) for s in range(3)]
+    caps = [p[0].vision_k.shape[2] for p in pairs]
+    assert len(set(caps)) == 1
+    batch = gdec.stack_caches([p[0] for p in pairs])
+    logs = [oatt.FetchLog() for _ in pairs]
+    for step in range(4):
+        q = np.stack([p[2][step][0] for p in pairs])
+        out, flags = gdec.decode_attention(dev(q), batch, 0.08)
+        for s, (c, oc, tr, rep) in enumerate(pairs):
+            o_ref, f_ref = oatt.decode_step(tr[step][0], oc, 0.08, rep, True, logs[s])
+            np.testing.assert_array_equal(flags[s].cpu().numpy().astype(bool), f_ref)
+            np.testing.assert_allclose(out[s].cpu().numpy(), np.stack(o_ref), atol=1e-3, rtol=1e-3)
+            oatt.append_answer(oc, tr[step][1], tr[step][2], 128)
+        ks = dev(np.stack([p[2][step][1] for p in pairs]))
+        vs = dev(np.stack([p[2][step][2] for p in pairs]))
+        gdec.append_answer(batch, ks, vs)
+    assert batch.fetch.vision_tokens == sum(l.vision_tokens for l in logs)
