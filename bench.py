@@ -1,0 +1,539 @@
+#!/usr/bin/env python
+"""Benchmark of the OmniSparse sparse-attention hot path on B200.
+
+Headline (BASELINE.json ``metric``): prefill sparse-attention throughput of a
+Qwen2-7B-shaped attention layer (28 Q / 4 KV heads, d=128) at 64K tokens
+(65472 vision + 64 text, config C3 at 1 GPU), plus the speed-up over the
+fastest dense causal bf16 flash-attention on the same GPU, and batch-32 decode
+tok/s and KV bytes per step over the slimmed cache (C5 shape, 1 GPU).
+
+One "step" = one full sparse prefill of the layer (K1 probe keys, K2 query
+scoring, row compaction, K3 probe mass + selection, K6 KV regroup, K4
+tcgen05 sparse attention) on HBM-resident synthetic inputs (Q alone is
+470 MB > 126 MB L2, so no flush is needed between steps).
+
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+Multi-GPU: torchrun --nproc-per-node N bench.py --gpus N (head-sharded, one
+all_gather of block masses per step; strong scaling).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "prefill sparse-attn latency @64K tok vs dense FA (×), decode tok/s & KV bytes"
+HQ, HKV, D = 28, 4, 128
+N_TEXT = 64
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--seq", type=int, default=65536)
+    ap.add_argument("--lazy", type=float, default=0.5)
+    ap.add_argument("--tau", type=float, default=0.08)
+    ap.add_argument("--p", type=float, default=0.82)
+    ap.add_argument("--decode-batch", type=int, default=32)
+    ap.add_argument("--no-decode", action="store_true")
+    ap.add_argument("--no-dense", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-knobs", action="store_true", help="skip the second-operating-point sweep")
+    ap.add_argument("--flashinfer", action="store_true", help="also time flashinfer's dense FMHA (JIT)")
+    return ap.parse_args()
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), float(p["bf16_tflops"]), float(p.get("bf16_tflops_sustained", p["bf16_tflops"])), "measured"
+    except Exception:
+        return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int = 0):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+            time.sleep(0.25)
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = sorted(float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit())
+        mx = max((float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()), default=None)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 2 + i and r[2 + i] == "Active"})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------------ timing
+def time_cuda(fn, steps: int, warmup: int, stream=None):
+    import torch
+
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record(stream)
+    for _ in range(steps):
+        fn()
+    e.record(stream)
+    torch.cuda.synchronize()
+    return s.elapsed_time(e) / steps
+
+
+def count_launches(fn) -> int:
+    """Kernels one call of fn launches (torch.profiler / CUPTI)."""
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        fn()
+        torch.cuda.synchronize()
+    names = [ev.name for ev in prof.events() if ev.device_type == torch.autograd.DeviceType.CUDA]
+    ours = [n for n in names if "omni" in n]
+    return len(ours), len(names), sorted(set(ours))
+
+
+def work_flops(res, n_kv_heads: int, d: int = D) -> float:
+    """Algorithmic forward FLOPs = 4 d sum_h sum_{r in A_h} |{j in S_g : j <= r}|
+    (SURVEY §8d), counted exactly from the produced index sets."""
+    import torch
+
+    hq = res.rows.shape[0]
+    rep = hq // n_kv_heads
+    counts = res.counts.cpu().tolist()
+    b = res.selection.info[4:].cpu().tolist()
+    total = 0
+    for h in range(hq):
+        g = h // rep
+        sel = res.selection.selected[g, : b[g]].contiguous()
+        rows = res.rows[h, : counts[h]].contiguous()
+        total += int(torch.searchsorted(sel, rows, right=True).sum())
+    return 4.0 * d * total
+
+
+# ------------------------------------------------------------------ dense FA baselines
+def dense_baselines(Q, K, V, steps, warmup, use_flashinfer=False):
+    import torch
+
+    hq, n, d = Q.shape
+    out = {}
+    q4, k4, v4 = Q.unsqueeze(0), K.unsqueeze(0), V.unsqueeze(0)
+    try:
+        from torch.nn.attention import SDPBackend, sdpa_kernel
+
+        def cudnn():
+            with sdpa_kernel(SDPBackend.CUDNN_ATTENTION):
+                return torch.nn.functional.scaled_dot_product_attention(q4, k4, v4, is_causal=True, enable_gqa=True)
+        cudnn()
+        out["cudnn_sdpa_ms"] = time_cuda(cudnn, steps, warmup)
+    except Exception as e:  # noqa: BLE001
+        out["cudnn_sdpa_error"] = str(e)[:160]
+    try:
+        from flash_attn import flash_attn_func
+
+        qf, kf, vf = (x.transpose(0, 1).unsqueeze(0).contiguous() for x in (Q, K, V))
+        fa = lambda: flash_attn_func(qf, kf, vf, causal=True)
+        fa()
+        out["flash_attn2_ms"] = time_cuda(fa, steps, warmup)
+        del qf, kf, vf
+    except Exception as e:  # noqa: BLE001
+        out["flash_attn2_error"] = str(e)[:160]
+    if use_flashinfer:
+        try:
+            import flashinfer
+
+            qf, kf, vf = (x.transpose(0, 1).contiguous() for x in (Q, K, V))
+            fi = lambda: flashinfer.single_prefill_with_kv_cache(qf, kf, vf, causal=True)
+            fi()
+            out["flashinfer_ms"] = time_cuda(fi, steps, warmup)
+        except Exception as e:  # noqa: BLE001
+            out["flashinfer_error"] = str(e)[:160]
+    times = {k: v for k, v in out.items() if k.endswith("_ms")}
+    if times:
+        best = min(times, key=times.get)
+        out["fastest"] = best[:-3]
+        out["fastest_ms"] = times[best]
+    out["dense_causal_flops"] = 4.0 * d * hq * n * (n + 1) / 2
+    return out
+
+
+# ------------------------------------------------------------------ CPU reference sample
+def cpu_reference_sample(Q, K, V, n_vision, tau, p, head=13, rows_sample=1024, seed=0):
+    """The oracle (float64 NumPy restatement of the reference path) timed on a
+    bounded sample of the SAME workload: the full selection pass over all 28
+    heads, then sparse_head_attention for `rows_sample` uniformly drawn active
+    rows of one head; the attention time is extrapolated to every active row of
+    every head. Returns (tok/s, seconds per full step, sample description)."""
+    import numpy as np
+
+    from oracle import attention as oatt
+    from oracle import pipeline as opipe
+
+    to64 = lambda t: t.float().cpu().numpy().astype(np.float64)
+    Qh, Kh, Vh = to64(Q), to64(K), to64(V)
+    n = Qh.shape[1]
+    t0 = time.perf_counter()
+    ref = opipe.select(Qh, Kh, n_vision, 0, tau, p, 256)
+    t_sel = time.perf_counter() - t0
+    rep = Qh.shape[0] // Kh.shape[0]
+    rows = np.flatnonzero(ref.active[head])
+    samp = np.sort(np.random.default_rng(seed).choice(rows, min(rows_sample, rows.size), replace=False))
+    t0 = time.perf_counter()
+    oatt.sparse_head_attention(Qh[head], Kh[head // rep], Vh[head // rep], ref.selected[head // rep],
+                               ref.active[head], 0, rows_subset=samp)
+    t_att = time.perf_counter() - t0
+    total_rows = int(ref.active.sum())
+    t_step = t_sel + t_att * total_rows / samp.size
+    desc = (f"oracle (NumPy f64 restatement of slimattn) on the same {n}-token workload: full selection over "
+            f"{Qh.shape[0]} heads ({t_sel:.2f} s) + sparse_head_attention of {samp.size} random active rows of head "
+            f"{head} ({t_att:.2f} s), extrapolated to all {total_rows} active rows")
+    return n / t_step, t_step, desc, ref
+
+
+# ------------------------------------------------------------------ decode
+def decode_section(args, steps, warmup, hbm_peak):
+    import torch
+
+    from paper_2511_12201_b200 import decode as gdec
+    from paper_2511_12201_b200 import ops
+    from paper_2511_12201_b200.pipeline import SparsityConfig, select_device
+    from paper_2511_12201_b200.synthetic import decode_queries_device, generate_device, unit_vision_mean
+
+    n = args.seq
+    nv = n - N_TEXT
+    B = args.decode_batch
+    cfg = SparsityConfig(tau=args.tau, p=args.p)
+    caches, k_means = [], []
+    for s in range(B):
+        Q, K, V = generate_device(HQ, HKV, D, nv, N_TEXT, seed=1000 + s, lazy_fraction=args.lazy)
+        k_lazy, k_act, pk, active, _, pq, rows, counts, mass, sel = select_device(Q, K, nv, cfg)
+        b = int(sel.info[0])
+        vsel = ops.select(mass, HKV, n, cfg.block_size, cfg.p, "token", vision_limit=nv, budget_override=b)
+        bv = min(b, nv)
+        caches.append(gdec.build_cache(K, V, vsel.selected, bv, nv, N_TEXT, k_lazy, k_act, HQ,
+                                       answer_capacity=warmup + steps + 8))
+        k_means.append(unit_vision_mean(K, nv))
+        del Q, K, V, pq, pk, rows, active
+    torch.cuda.empty_cache()
+    cache = gdec.stack_caches(caches)
+    del caches
+    torch.cuda.empty_cache()
+    n_steps = warmup + steps
+    qs = [decode_queries_device(HQ, HKV, k_means, range(B), args.lazy, t) for t in range(n_steps)]
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(7)
+    kv_new = [(torch.randn(B, HKV, D, generator=gen, device="cuda").bfloat16(),
+               torch.randn(B, HKV, D, generator=gen, device="cuda").bfloat16()) for _ in range(n_steps)]
+    flags_log = []
+
+    def step(t):
+        out, fl = gdec.decode_attention(qs[t], cache, args.tau, log=False)
+        flags_log.append(fl)
+        gdec.append_answer(cache, *kv_new[t])
+
+    for t in range(warmup):
+        step(t)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    flags_log.clear()
+    e0.record()
+    for t in range(warmup, n_steps):
+        step(t)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    # bytes each timed step read (vision of fetched groups + text + answer), bf16
+    n_ans0 = cache.n_answer - steps
+    tot_vis, tot_ta = 0, 0
+    for i, fl in enumerate(flags_log):
+        vt, vb, _ = gdec.step_bytes(cache, fl)
+        tot_vis += vb
+        tot_ta += B * HKV * (N_TEXT + n_ans0 + i) * 2 * D * 2
+    slim_bytes = (tot_vis + tot_ta) / steps
+    full_bytes = B * HKV * (n + n_ans0 + steps / 2) * 2 * D * 2
+    q_bytes = B * HQ * D * (2 + 4)
+    res = {
+        "batch": B, "context": n, "ms_per_step": ms, "tok_s": B / (ms / 1e3),
+        "kv_bytes_per_step": slim_bytes, "full_cache_bytes_per_step": full_bytes,
+        "kv_bytes_reduction": full_bytes / slim_bytes,
+        "budgets_mean": sum(cache.budgets) / B,
+        "fetched_group_frac": float(torch.stack([f.view(B, HKV, -1).any(dim=2) for f in flags_log]).float().mean()),
+        "roofline": {"bound": "hbm", "achieved": (slim_bytes + q_bytes) / (ms / 1e3) / 1e9, "peak": hbm_peak,
+                     "unit": "GB/s", "frac": (slim_bytes + q_bytes) / (ms / 1e3) / 1e9 / hbm_peak},
+    }
+    # dense full-cache decode baseline (flash-attn kv-cache kernel), same batch/context
+    try:
+        from flash_attn import flash_attn_with_kvcache
+
+        del cache
+        torch.cuda.empty_cache()
+        kc = torch.randn(B, n, HKV, D, device="cuda", dtype=torch.bfloat16)
+        vc = torch.randn(B, n, HKV, D, device="cuda", dtype=torch.bfloat16)
+        q1 = torch.randn(B, 1, HQ, D, device="cuda", dtype=torch.bfloat16)
+        lens = torch.full((B,), n, dtype=torch.int32, device="cuda")
+        fn = lambda: flash_attn_with_kvcache(q1, kc, vc, cache_seqlens=lens)
+        dms = time_cuda(fn, steps, warmup)
+        res["dense_decode"] = {"kernel": "flash_attn_with_kvcache (full cache)", "ms_per_step": dms,
+                               "tok_s": B / (dms / 1e3)}
+        res["speedup_vs_dense_decode"] = dms / ms
+        del kc, vc
+    except Exception as e:  # noqa: BLE001
+        res["dense_decode_error"] = str(e)[:160]
+    return res
+
+
+# ------------------------------------------------------------------ main arms
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2511_12201_b200 import ops
+    from paper_2511_12201_b200.parallel import shard_plan, sparse_prefill_sharded
+    from paper_2511_12201_b200.pipeline import SparsityConfig, select_device, sparse_prefill_device
+    from paper_2511_12201_b200.synthetic import generate_device
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    ops.device_check()
+    hbm_peak, tc_peak, tc_sus, peak_src = peaks()
+    n, nv = args.seq, args.seq - N_TEXT
+    cfg = SparsityConfig(tau=args.tau, p=args.p)
+    Q, K, V = generate_device(HQ, HKV, D, nv, N_TEXT, seed=0, lazy_fraction=args.lazy)
+    plan = shard_plan(HQ, HKV, world, rank)
+    if world > 1:
+        Ql = Q[plan.q_start:plan.q_stop].contiguous()
+        Kl = K[plan.g_start:plan.g_stop].contiguous()
+        Vl = V[plan.g_start:plan.g_stop].contiguous()
+        O = torch.empty_like(Ql)
+        step = lambda: sparse_prefill_sharded(Ql, Kl, Vl, plan, nv, world, cfg, out=O)
+    else:
+        O = torch.empty_like(Q)
+        step = lambda: sparse_prefill_device(Q, K, V, nv, cfg, out=O)
+
+    res = step()
+    torch.cuda.synchronize()
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.steps):
+            res = step()
+        e1.record()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t)
+    value = n / (ms / 1e3)
+    line = {"metric": METRIC, "value": value, "unit": "tok/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic: reference generator construction (workload.py:88-129, GQA rule B) drawn with torch CUDA RNG",
+            "config": {"workload": f"Qwen2-7B-shaped attention layer sparse prefill, {HQ} Q / {HKV} KV heads, d={D}, "
+                                   f"{n} tokens ({nv} vision + {N_TEXT} text)",
+                       "knobs": {"tau": args.tau, "p": args.p, "block_size": 256, "lazy_fraction": args.lazy,
+                                 "granularity": "token", "preserve_first_head": True},
+                       "parallelism": f"head-sharded x{world}" if world > 1 else "single GPU",
+                       "l2": "inputs larger than L2 (Q alone 470 MB at 64K); no flush"}}
+    line["clocks"] = clk.summary()
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    b = int(res.selection.info[0])
+    flops = work_flops(res, HKV) if world == 1 else None
+    line["selection"] = {"budget": b, "b_over_n": b / n, "flattest_group": int(res.selection.info[1]),
+                         "active_frac": float(res.active.float().mean())}
+    if world == 1:
+        line["selection"]["work_ratio_vs_dense_causal"] = flops / (4.0 * D * HQ * n * (n + 1) / 2)
+        # ----- per-kernel breakdown and the K4 roofline (dominant kernel, own stream events)
+        rows, counts, sel = res.rows, res.counts, res.selection
+        fa = lambda: ops.sparse_attn_fwd(Q, res.K_sel, res.V_sel, V, rows, counts, sel.selected, sel.counts, 0, O,
+                                         res.lse)
+        fa_ms = time_cuda(fa, args.steps, 2)
+        sel_ms = time_cuda(lambda: select_device(Q, K, nv, cfg, O_zero=O), args.steps, 2)
+        cap = ops.round_up(n, 128)
+        gat_ms = time_cuda(lambda: (ops.gather_rows(K, sel.selected, sel.counts, cap, 128, out=res.K_sel),
+                                    ops.gather_rows(V, sel.selected, sel.counts, cap, 128, out=res.V_sel)),
+                           args.steps, 2)
+        achieved = flops / (fa_ms / 1e3) / 1e12
+        line["roofline"] = {"bound": "tensor", "kernel": "omni sparse_fwd_kernel (K4)", "achieved": achieved,
+                            "peak": tc_peak, "unit": "TFLOP/s", "frac": achieved / tc_peak, "traffic": None,
+                            "peak_source": f"{peak_src} bf16 burst (MEASURED_PEAKS.json)",
+                            "algorithmic_flops_per_launch": flops, "launch_ms": fa_ms}
+        line["breakdown_ms"] = {"select_path_K1_K2_compact_K3": sel_ms, "gather_K6": gat_ms, "sparse_fa_K4": fa_ms,
+                                "k4_share_of_step": fa_ms / ms}
+        n_ours, n_all, names = count_launches(step)
+        line["gpu_launches"] = n_ours * args.steps
+        line["gpu_launches_per_step"] = {"ours": n_ours, "all": n_all, "kernels": names}
+        # ----- dense FA comparators on the same tensors
+        if not args.no_dense:
+            dense = dense_baselines(Q, K, V, args.steps, 2, args.flashinfer)
+            line["dense_fa"] = dense
+            if "fastest_ms" in dense:
+                line["speedup_vs_dense_fa"] = dense["fastest_ms"] / ms
+                line["dense_fa_tflops"] = dense["dense_causal_flops"] / (dense["fastest_ms"] / 1e3) / 1e12
+        # ----- second operating point (paper's tau=0.12, p=0.75) and lazier workload
+        if not args.no_knobs and not args.no_dense and "fastest_ms" in line.get("dense_fa", {}):
+            sweep = []
+            for lz, tau, p in ((0.5, 0.12, 0.75), (0.7, 0.08, 0.82), (0.7, 0.12, 0.75)):
+                Q2, K2, V2 = generate_device(HQ, HKV, D, nv, N_TEXT, seed=0, lazy_fraction=lz)
+                c2 = SparsityConfig(tau=tau, p=p)
+                O2 = torch.empty_like(Q2)
+                st2 = lambda: sparse_prefill_device(Q2, K2, V2, nv, c2, out=O2)
+                r2 = st2()
+                ms2 = time_cuda(st2, args.steps, 2)
+                sweep.append({"lazy_fraction": lz, "tau": tau, "p": p, "ms_per_step": ms2,
+                              "speedup_vs_dense_fa": line["dense_fa"]["fastest_ms"] / ms2,
+                              "budget": int(r2.selection.info[0]),
+                              "work_ratio": work_flops(r2, HKV) / (4.0 * D * HQ * n * (n + 1) / 2)})
+                del Q2, K2, V2, O2, r2
+            line["knob_sweep"] = sweep
+        # ----- end-to-end through the public API with host buffers
+        if not args.no_e2e:
+            hQ, hK, hV = (x.cpu().pin_memory() for x in (Q, K, V))
+            hO = torch.empty(Q.shape, dtype=torch.bfloat16).pin_memory()
+
+            def e2e():
+                Q.copy_(hQ, non_blocking=True)
+                K.copy_(hK, non_blocking=True)
+                V.copy_(hV, non_blocking=True)
+                sparse_prefill_device(Q, K, V, nv, cfg, out=O)
+                hO.copy_(O, non_blocking=True)
+
+            e_ms = time_cuda(e2e, max(3, args.steps // 2), 1)
+            h2d = sum(x.numel() * x.element_size() for x in (hQ, hK, hV))
+            line["e2e"] = {"value": n / (e_ms / 1e3), "unit": "tok/s", "ms_per_step": e_ms,
+                           "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": hO.numel() * hO.element_size(),
+                           "api": "pipeline.sparse_prefill_device with pinned host Q/K/V in, O out"}
+        # ----- CPU reference path on the host cores (bounded sample)
+        if not args.no_cpu:
+            try:
+                tps, t_step, desc, _ = cpu_reference_sample(Q, K, V, nv, args.tau, args.p)
+                line["cpu_baseline"] = {"value": tps, "unit": "tok/s", "cores": os.cpu_count(), "kind": "port",
+                                        "seconds_per_step_extrapolated": t_step, "sample": desc}
+            except Exception as e:  # noqa: BLE001
+                line["cpu_baseline"] = {"error": str(e)[:200]}
+        # ----- decode (C5 shape at 1 GPU, sequence-sharded across ranks at N>1)
+        if not args.no_decode:
+            del res
+            torch.cuda.empty_cache()
+            try:
+                line["decode"] = decode_section(args, args.steps, args.warmup, hbm_peak)
+            except Exception as e:  # noqa: BLE001
+                line["decode"] = {"error": str(e)[:300]}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def run_reference(args):
+    """--impl reference: the reference's CPU path (its NumPy restatement in
+    oracle/, float64, all host threads) on this arm's config and metric; rank 0
+    only. Each step = selection over the full 64K workload + a bounded
+    attention sample extrapolated to the whole layer."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import torch
+
+    from paper_2511_12201_b200.synthetic import generate_device
+
+    n, nv = args.seq, args.seq - N_TEXT
+    Q, K, V = generate_device(HQ, HKV, D, nv, N_TEXT, seed=0, lazy_fraction=args.lazy, device="cpu")
+    times = []
+    desc = ""
+    for i in range(args.warmup + args.steps):
+        tps, t_step, desc, _ = cpu_reference_sample(Q, K, V, nv, args.tau, args.p, rows_sample=256, seed=i)
+        if i >= args.warmup:
+            times.append(t_step)
+    ms = 1e3 * sum(times) / len(times)
+    value = n / (ms / 1e3)
+    line = {"metric": METRIC, "value": value, "unit": "tok/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "impl": "reference",
+            "data": "synthetic: reference generator construction, torch CPU RNG",
+            "config": {"workload": f"Qwen2-7B-shaped attention layer sparse prefill, {HQ} Q / {HKV} KV heads, d={D}, "
+                                   f"{n} tokens ({nv} vision + {N_TEXT} text)",
+                       "knobs": {"tau": args.tau, "p": args.p, "block_size": 256, "lazy_fraction": args.lazy}},
+            "cpu_baseline": {"value": value, "unit": "tok/s", "cores": os.cpu_count(), "kind": "port",
+                             "sample": desc},
+            "e2e": {"value": value, "unit": "tok/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -70,22 +70,25 @@ def generate_device(hq: int, hkv: int, d: int, n_vision: int, n_text: int, seed:
     return Q, K, V
 
 
-def decode_queries_device(hq: int, hkv: int, K: torch.Tensor, n_vision: int, batch_seeds, lazy_fraction: float,
-                          step: int, dtype=torch.bfloat16):
+def decode_queries_device(hq: int, hkv: int, u_content: list, seeds, lazy_fraction: float, step: int,
+                          dtype=torch.bfloat16):
     """``workload.py:132-157`` on the device: one decoding query per Q head,
-    lazy with probability ``lazy_fraction``. K is [B, hkv, N, d] or a list of
-    per-sequence [hkv, N, d] tensors (only the vision mean is used)."""
+    lazy with probability ``lazy_fraction``, aligned (+ACTIVE_ALIGN) or
+    anti-aligned (-LAZY_ANTI_ALIGN) with its group's unit vision-key mean.
+    u_content: per sequence [hkv, d] unit vectors. Returns [B, hq, d]."""
     rep = hq // hkv
     qs = []
-    for s, seed in enumerate(batch_seeds):
-        gen = torch.Generator(device=K[s].device)
-        gen.manual_seed(10_000 * seed + step)
-        u = K[s][:, :n_vision].float().mean(dim=1)
-        u = u / u.norm(dim=1, keepdim=True)
+    for u, seed in zip(u_content, seeds):
+        gen = torch.Generator(device=u.device)
+        gen.manual_seed(10_000 * int(seed) + step)
         q = torch.randn(hq, u.shape[1], generator=gen, device=u.device)
         lazy = torch.rand(hq, generator=gen, device=u.device) < lazy_fraction
-        coef = torch.where(lazy, torch.tensor(-LAZY_ANTI_ALIGN, device=u.device),
-                           torch.tensor(ACTIVE_ALIGN, device=u.device))
+        coef = torch.where(lazy, torch.full_like(q[:, 0], -LAZY_ANTI_ALIGN), torch.full_like(q[:, 0], ACTIVE_ALIGN))
         q += coef[:, None] * u.repeat_interleave(rep, dim=0)
         qs.append(q)
     return torch.stack(qs).to(dtype)
+
+
+def unit_vision_mean(K: torch.Tensor, n_vision: int) -> torch.Tensor:
+    m = K[:, :n_vision].float().mean(dim=1)
+    return m / m.norm(dim=1, keepdim=True)
