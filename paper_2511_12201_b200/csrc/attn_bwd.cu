@@ -1,14 +1,623 @@
-// K5: backward of the gathered sparse flash attention (placeholder until the
-// tcgen05 backward lands; returns PARAM so callers fail loudly).
+// K5: backward of the gathered sparse flash attention (tcgen05 / TMEM / TMA).
+//
+// The reference has no autograd; gradients are checked against a float64
+// torch-autograd restatement of sparse_head_attention (oracle/grad.py). With
+// compacted active rows (per Q head) and compacted selected keys (per group):
+//   P_ij  = exp(s_ij - lse_i) for j < vis_i (original-position staircase)
+//   dV_j  = sum_i P_ij dO_i            dP_ij = dO_i . V_j
+//   dS_ij = P_ij (dP_ij - D_i)          D_i   = dO_i . O_i
+//   dQ_i  = scale sum_j dS_ij K_j       dK_j  = scale sum_i dS_ij Q_i
+// Rows with no visible key copied V[sink] in the forward: their dO goes to
+// dV[sink] (dV_sink). Three kernels, no atomics on the hot path:
+//   prep  (HBM-bound): gathers Q / dO rows into compact bf16 tiles, computes
+//         D_i, log2-domain LSE and vis_i per compact row;
+//   dq    Q-tile CTAs (like the forward): S = Q K^T, dP = dO V^T, dS -> smem,
+//         dQ += dS K (TMEM accumulator);
+//   dkv   KV-tile CTAs looping over every Q tile of the group's Q heads that
+//         can see the tile: S^T = K Q^T, dP^T = V dO^T, P^T / dS^T -> smem,
+//         dV += P^T dO, dK += dS^T Q (TMEM accumulators). GQA accumulation over
+//         the group's Q heads happens inside one CTA (deterministic).
+#include <math.h>
+
 #include "common.cuh"
 
-extern "C" size_t omni_sparse_attn_bwd_workspace(int n_q_heads, int seq_len) {
-  return 16;
+namespace omni {
+namespace bwd {
+
+constexpr int D = 128;
+constexpr uint32_t ATOM = 128 * 128;  // 128 rows x 128 B swizzle region
+constexpr uint32_t TILE = 2 * ATOM;   // 128 x 128 bf16
+
+__device__ __forceinline__ uint32_t swz(uint32_t row, uint32_t chunk16) {
+  return row * 128u + ((chunk16 ^ (row & 7u)) << 4);
 }
 
-extern "C" int omni_sparse_attn_bwd(const void*, const void*, const void*, const void*, const void*, const float*,
-                                    const int32_t*, const int32_t*, const int32_t*, const int32_t*, int, int, int,
-                                    int, int, float*, float*, float*, float*, void*, void*) {
-  OMNI_CHECK(false, OMNI_E_PARAM, "sparse attention backward not built yet");
-  return OMNI_OK;
+// ------------------------------------------------------------------ prep
+__global__ void __launch_bounds__(256) bwd_prep_kernel(
+    const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __restrict__ O, const __nv_bfloat16* __restrict__ dO,
+    const float* __restrict__ lse, const int32_t* __restrict__ rows, const int32_t* __restrict__ counts,
+    const int32_t* __restrict__ sel, const int32_t* __restrict__ sel_counts, int N, int rep, int capq,
+    __nv_bfloat16* __restrict__ Qc, __nv_bfloat16* __restrict__ dOc, float* __restrict__ lse2c,
+    float* __restrict__ Dc, int32_t* __restrict__ visc, float* __restrict__ dv_sink) {
+  const int h = blockIdx.y;
+  const int i = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  const int cnt = __ldg(counts + h);
+  const int lim = ((cnt + 127) / 128) * 128;
+  if (i >= lim) return;
+  const size_t ci = (size_t)h * capq + i;
+  uint2* qd = reinterpret_cast<uint2*>(Qc + ci * D);
+  uint2* dd = reinterpret_cast<uint2*>(dOc + ci * D);
+  if (i >= cnt) {
+    qd[lane] = make_uint2(0, 0);
+    dd[lane] = make_uint2(0, 0);
+    if (lane == 0) {
+      lse2c[ci] = 0.f;
+      Dc[ci] = 0.f;
+      visc[ci] = 0;
+    }
+    return;
+  }
+  const int g = h / rep;
+  const int pos = __ldg(rows + (size_t)h * N + i);
+  const size_t src = ((size_t)h * N + pos) * D;
+  const uint2 qv = __ldg(reinterpret_cast<const uint2*>(Q + src) + lane);
+  const uint2 ov = __ldg(reinterpret_cast<const uint2*>(O + src) + lane);
+  const uint2 gv = __ldg(reinterpret_cast<const uint2*>(dO + src) + lane);
+  qd[lane] = qv;
+  dd[lane] = gv;
+  const __nv_bfloat162* o2 = reinterpret_cast<const __nv_bfloat162*>(&ov);
+  const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&gv);
+  float dsum = 0.f;
+  float gf[4];
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const float2 a = __bfloat1622float2(o2[k]), b = __bfloat1622float2(g2[k]);
+    dsum += a.x * b.x + a.y * b.y;
+    gf[2 * k] = b.x;
+    gf[2 * k + 1] = b.y;
+  }
+  dsum = warp_sum(dsum);
+  int vis = 0;
+  if (lane == 0) {
+    vis = count_le(sel + (size_t)g * N, __ldg(sel_counts + g), pos);
+    Dc[ci] = dsum;
+    lse2c[ci] = __ldg(lse + (size_t)h * N + pos) * static_cast<float>(kLog2e);
+    visc[ci] = vis;
+  }
+  vis = __shfl_sync(0xffffffffu, vis, 0);
+  if (vis == 0) {  // forward copied V[sink] for this row: dV[sink] += dO
+#pragma unroll
+    for (int k = 0; k < 4; ++k) atomicAdd(dv_sink + (size_t)g * D + lane * 4 + k, gf[k]);
+  }
+}
+
+// ------------------------------------------------------------------ dq
+namespace dq {
+constexpr uint32_t OFF_Q = 0, OFF_DO = TILE, OFF_K = 2 * TILE, OFF_V = 4 * TILE, OFF_DS = 6 * TILE;
+constexpr uint32_t OFF_BAR = 7 * TILE;
+enum { B_QD = 0, B_KF = 1, B_KE = 3, B_VF = 5, B_VE = 7, B_SF = 9, B_SE = 10, B_DSF = 11, B_DSE = 12, B_N = 13 };
+constexpr uint32_t OFF_TMEM = OFF_BAR + 8 * B_N;
+constexpr uint32_t SMEM = OFF_TMEM + 16 + 1024;
+constexpr uint32_t COL_S = 0, COL_DP = 128, COL_DQ = 256;
+}  // namespace dq
+
+__global__ void __launch_bounds__(256, 1)
+dq_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
+          const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
+          const int32_t* __restrict__ rows, const int32_t* __restrict__ counts, const float* __restrict__ lse2c,
+          const float* __restrict__ Dc, const int32_t* __restrict__ visc, int Hq, int rep, int N, int cap, int capq,
+          int n_tiles, float* __restrict__ dQ) {
+  using namespace dq;
+  extern __shared__ uint8_t smem_raw[];
+  const int L = blockIdx.x;
+  const int h = L % Hq;
+  const int tile = n_tiles - 1 - L / Hq;
+  const int cnt = __ldg(counts + h);
+  const int r0 = tile * 128;
+  if (r0 >= cnt) return;
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sb = smem_u32(smem);
+  const uint32_t bar = sb + OFF_BAR;
+  auto B = [&](int i) { return bar + 8u * i; };
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + OFF_TMEM);
+  __shared__ int s_nt;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = h / rep;
+  const int nrows = min(128, cnt - r0);
+  const size_t crow0 = (size_t)h * capq + r0;
+  if (threadIdx.x == 0) {
+    s_nt = (__ldg(visc + crow0 + nrows - 1) + 127) / 128;
+    tma_prefetch_desc(&tm_q);
+    tma_prefetch_desc(&tm_do);
+    tma_prefetch_desc(&tm_k);
+    tma_prefetch_desc(&tm_v);
+    mbar_init(B(B_QD), 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(B(B_KF + s), 1);
+      mbar_init(B(B_KE + s), 1);
+      mbar_init(B(B_VF + s), 1);
+      mbar_init(B(B_VE + s), 1);
+    }
+    mbar_init(B(B_SF), 1);
+    mbar_init(B(B_SE), 128);
+    mbar_init(B(B_DSF), 128);
+    mbar_init(B(B_DSE), 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) {
+    tmem_alloc(smem_u32(tmem_slot), 512);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int nt = s_nt;
+
+  if (warp == 0) {
+    if (lane == 0 && nt > 0) {
+      mbar_expect_tx(B(B_QD), 2 * TILE);
+      tma_load_2d(sb + OFF_Q, &tm_q, B(B_QD), 0, (int)crow0);
+      tma_load_2d(sb + OFF_Q + ATOM, &tm_q, B(B_QD), 64, (int)crow0);
+      tma_load_2d(sb + OFF_DO, &tm_do, B(B_QD), 0, (int)crow0);
+      tma_load_2d(sb + OFF_DO + ATOM, &tm_do, B(B_QD), 64, (int)crow0);
+      const int kr0 = g * cap;
+      for (int j = 0; j < nt; ++j) {
+        const int s = j & 1;
+        if (j >= 2) mbar_wait(B(B_KE + s), ((j >> 1) - 1) & 1);
+        mbar_expect_tx(B(B_KF + s), TILE);
+        tma_load_2d(sb + OFF_K + s * TILE, &tm_k, B(B_KF + s), 0, kr0 + j * 128);
+        tma_load_2d(sb + OFF_K + s * TILE + ATOM, &tm_k, B(B_KF + s), 64, kr0 + j * 128);
+        if (j >= 2) mbar_wait(B(B_VE + s), ((j >> 1) - 1) & 1);
+        mbar_expect_tx(B(B_VF + s), TILE);
+        tma_load_2d(sb + OFF_V + s * TILE, &tm_v, B(B_VF + s), 0, kr0 + j * 128);
+        tma_load_2d(sb + OFF_V + s * TILE + ATOM, &tm_v, B(B_VF + s), 64, kr0 + j * 128);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && nt > 0) {
+      constexpr uint32_t id_kk = idesc_bf16_f32(128, 128, 0, 0);
+      constexpr uint32_t id_mn = idesc_bf16_f32(128, 128, 0, 1);
+      auto issue_s = [&](int j) {
+        const int s = j & 1;
+        mbar_wait(B(B_KF + s), (j >> 1) & 1);
+        mbar_wait(B(B_VF + s), (j >> 1) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t off = (kk >> 2) * ATOM + (kk & 3) * 32;
+          umma_bf16(tmem + COL_S, sdesc_sw128(sb + OFF_Q + off, 16, 1024),
+                    sdesc_sw128(sb + OFF_K + s * TILE + off, 16, 1024), id_kk, kk > 0);
+        }
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t off = (kk >> 2) * ATOM + (kk & 3) * 32;
+          umma_bf16(tmem + COL_DP, sdesc_sw128(sb + OFF_DO + off, 16, 1024),
+                    sdesc_sw128(sb + OFF_V + s * TILE + off, 16, 1024), id_kk, kk > 0);
+        }
+        umma_commit(B(B_VE + s));
+        umma_commit(B(B_SF));
+      };
+      mbar_wait(B(B_QD), 0);
+      issue_s(0);
+      for (int j = 0; j < nt; ++j) {
+        mbar_wait(B(B_SE), j & 1);
+        if (j + 1 < nt) issue_s(j + 1);
+        mbar_wait(B(B_DSF), j & 1);
+        tc_fence_after();
+        const uint32_t kb = sb + OFF_K + (j & 1) * TILE;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          umma_bf16(tmem + COL_DQ, sdesc_sw128(sb + OFF_DS + (kk >> 2) * ATOM + (kk & 3) * 32, 16, 1024),
+                    sdesc_sw128(kb + kk * 2048, ATOM, 1024), id_mn, (j > 0 || kk > 0) ? 1u : 0u);
+        }
+        umma_commit(B(B_KE + (j & 1)));
+        umma_commit(B(B_DSE));
+      }
+    }
+  } else if (warp >= 4) {
+    const int i = threadIdx.x - 128;
+    const bool valid = i < nrows;
+    const size_t ci = crow0 + i;
+    const int vis = valid ? __ldg(visc + ci) : 0;
+    const float l2 = valid ? __ldg(lse2c + ci) : 0.f;
+    const float Dv = valid ? __ldg(Dc + ci) : 0.f;
+    const uint32_t tl = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+    const float sl2 = static_cast<float>(kLog2e / sqrt(static_cast<double>(D)));
+    uint8_t* ds_gen = smem + OFF_DS;
+    for (int j = 0; j < nt; ++j) {
+      mbar_wait(B(B_SF), j & 1);
+      tc_fence_after();
+      if (j > 0) mbar_wait(B(B_DSE), (j - 1) & 1);  // dQ MMA of j-1 finished reading dS
+      const int lim = vis - j * 128;
+#pragma unroll
+      for (int c4 = 0; c4 < 4; ++c4) {
+        uint32_t s[32], p[32];
+        __syncwarp();
+        tmem_ld32(tl + COL_S + c4 * 32, s);
+        tmem_ld32(tl + COL_DP + c4 * 32, p);
+        tmem_wait_ld();
+        uint32_t pk[16];
+#pragma unroll
+        for (int c = 0; c < 32; c += 2) {
+          const int col = c4 * 32 + c;
+          const float p0 = (col < lim) ? fast_exp2(__uint_as_float(s[c]) * sl2 - l2) : 0.f;
+          const float p1 = (col + 1 < lim) ? fast_exp2(__uint_as_float(s[c + 1]) * sl2 - l2) : 0.f;
+          pk[c / 2] = pack_bf16x2(p0 * (__uint_as_float(p[c]) - Dv), p1 * (__uint_as_float(p[c + 1]) - Dv));
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int chunk = c4 * 4 + q;  // 16-byte chunk index along keys (0..15)
+          *reinterpret_cast<uint4*>(ds_gen + (chunk >> 3) * ATOM + swz(i, chunk & 7)) =
+              make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(B(B_SE));
+      fence_proxy_async_smem();
+      mbar_arrive(B(B_DSF));
+    }
+    if (nt > 0) {
+      mbar_wait(B(B_DSE), (nt - 1) & 1);
+      tc_fence_after();
+      const float scale = static_cast<float>(1.0 / sqrt(static_cast<double>(D)));
+      const int pos = valid ? __ldg(rows + (size_t)h * N + r0 + i) : 0;
+      float4* dst = reinterpret_cast<float4*>(dQ + ((size_t)h * N + pos) * D);
+#pragma unroll
+      for (int c4 = 0; c4 < 4; ++c4) {
+        uint32_t o[32];
+        __syncwarp();
+        tmem_ld32(tl + COL_DQ + c4 * 32, o);
+        tmem_wait_ld();
+        if (valid) {
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            dst[c4 * 8 + q] = make_float4(__uint_as_float(o[4 * q]) * scale, __uint_as_float(o[4 * q + 1]) * scale,
+                                          __uint_as_float(o[4 * q + 2]) * scale,
+                                          __uint_as_float(o[4 * q + 3]) * scale);
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    __syncwarp();
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+// ------------------------------------------------------------------ dkv
+namespace dkv {
+constexpr int BR = 64;                     // Q rows per inner tile
+constexpr uint32_t QATOM = BR * 128;       // 64 rows x 128 B
+constexpr uint32_t QTILE = 2 * QATOM;      // 64 x 128 bf16
+constexpr uint32_t OFF_K = 0, OFF_V = TILE, OFF_Q = 2 * TILE, OFF_DO = OFF_Q + 2 * QTILE;
+constexpr uint32_t OFF_PT = OFF_DO + 2 * QTILE;  // [128 keys][64 rows] bf16, one swizzle atom wide
+constexpr uint32_t OFF_DST = OFF_PT + 128 * 128;
+constexpr uint32_t OFF_INFO = OFF_DST + 128 * 128;  // [2][3][64] f32/i32
+constexpr uint32_t OFF_BAR = OFF_INFO + 2 * 3 * BR * 4;
+enum { B_KV = 0, B_QF = 1, B_QE = 3, B_IF = 5, B_IE = 7, B_SF = 9, B_SE = 10, B_PF = 11, B_PE = 12, B_N = 13 };
+constexpr uint32_t OFF_TMEM = OFF_BAR + 8 * B_N;
+constexpr uint32_t SMEM = OFF_TMEM + 16 + 1024;
+constexpr uint32_t COL_S = 0, COL_DP = 64, COL_DV = 128, COL_DK = 256;
+}  // namespace dkv
+
+// Iteration space of one KV tile: for each Q head of the group, the 64-row
+// compact Q tiles from the first row that can see the tile's first key.
+struct DkvIter {
+  int h0, rep, first_tile[16], n_tiles[16], total;
+};
+
+__global__ void __launch_bounds__(256, 1)
+dkv_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
+           const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
+           const int32_t* __restrict__ rows, const int32_t* __restrict__ counts, const int32_t* __restrict__ sel,
+           const int32_t* __restrict__ sel_counts, const float* __restrict__ lse2c, const float* __restrict__ Dc,
+           const int32_t* __restrict__ visc, int rep, int N, int cap, int capq, float* __restrict__ dK,
+           float* __restrict__ dV) {
+  using namespace dkv;
+  extern __shared__ uint8_t smem_raw[];
+  const int t = blockIdx.x, g = blockIdx.y;
+  const int nsel = __ldg(sel_counts + g);
+  const int k0 = t * 128;
+  if (k0 >= nsel) return;
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sb = smem_u32(smem);
+  const uint32_t bar = sb + OFF_BAR;
+  auto B = [&](int i) { return bar + 8u * i; };
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + OFF_TMEM);
+  __shared__ DkvIter it;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    const int first_key = __ldg(sel + (size_t)g * N + k0);
+    it.h0 = g * rep;
+    it.rep = rep;
+    int tot = 0;
+    for (int r = 0; r < rep; ++r) {
+      const int h = g * rep + r;
+      const int cnt = __ldg(counts + h);
+      // first compact row whose position >= first_key (it sees key k0)
+      const int32_t* rh = rows + (size_t)h * N;
+      int lo = 0, hi = cnt;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (__ldg(rh + mid) < first_key) lo = mid + 1; else hi = mid;
+      }
+      it.first_tile[r] = lo / BR;
+      it.n_tiles[r] = max(0, (cnt + BR - 1) / BR - lo / BR);
+      tot += it.n_tiles[r];
+    }
+    it.total = tot;
+    tma_prefetch_desc(&tm_q);
+    tma_prefetch_desc(&tm_do);
+    tma_prefetch_desc(&tm_k);
+    tma_prefetch_desc(&tm_v);
+    mbar_init(B(B_KV), 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(B(B_QF + s), 1);
+      mbar_init(B(B_QE + s), 1);
+      mbar_init(B(B_IF + s), 64);
+      mbar_init(B(B_IE + s), 128);
+    }
+    mbar_init(B(B_SF), 1);
+    mbar_init(B(B_SE), 128);
+    mbar_init(B(B_PF), 128);
+    mbar_init(B(B_PE), 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) {
+    tmem_alloc(smem_u32(tmem_slot), 512);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int total = it.total;
+  // iteration index -> (head, compact Q tile)
+  auto decode_it = [&](int k, int& h, int& qt) {
+    int r = 0;
+    while (k >= it.n_tiles[r]) { k -= it.n_tiles[r]; ++r; }
+    h = it.h0 + r;
+    qt = it.first_tile[r] + k;
+  };
+
+  if (warp == 0) {
+    if (lane == 0 && total > 0) {
+      mbar_expect_tx(B(B_KV), 2 * TILE);
+      const int kr = g * cap + k0;
+      tma_load_2d(sb + OFF_K, &tm_k, B(B_KV), 0, kr);
+      tma_load_2d(sb + OFF_K + ATOM, &tm_k, B(B_KV), 64, kr);
+      tma_load_2d(sb + OFF_V, &tm_v, B(B_KV), 0, kr);
+      tma_load_2d(sb + OFF_V + ATOM, &tm_v, B(B_KV), 64, kr);
+      for (int k = 0; k < total; ++k) {
+        const int s = k & 1;
+        int h, qt;
+        decode_it(k, h, qt);
+        const int row = h * capq + qt * BR;
+        if (k >= 2) mbar_wait(B(B_QE + s), ((k >> 1) - 1) & 1);
+        mbar_expect_tx(B(B_QF + s), 2 * QTILE);
+        tma_load_2d(sb + OFF_Q + s * QTILE, &tm_q, B(B_QF + s), 0, row);
+        tma_load_2d(sb + OFF_Q + s * QTILE + QATOM, &tm_q, B(B_QF + s), 64, row);
+        tma_load_2d(sb + OFF_DO + s * QTILE, &tm_do, B(B_QF + s), 0, row);
+        tma_load_2d(sb + OFF_DO + s * QTILE + QATOM, &tm_do, B(B_QF + s), 64, row);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && total > 0) {
+      constexpr uint32_t id_s = idesc_bf16_f32(128, BR, 0, 0);
+      constexpr uint32_t id_acc = idesc_bf16_f32(128, 128, 0, 1);
+      auto issue_s = [&](int k) {
+        const int s = k & 1;
+        mbar_wait(B(B_QF + s), (k >> 1) & 1);
+        tc_fence_after();
+        const uint32_t qb = sb + OFF_Q + s * QTILE, db = sb + OFF_DO + s * QTILE;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t oa = (kk >> 2) * ATOM + (kk & 3) * 32, ob = (kk >> 2) * QATOM + (kk & 3) * 32;
+          umma_bf16(tmem + COL_S, sdesc_sw128(sb + OFF_K + oa, 16, 1024), sdesc_sw128(qb + ob, 16, 1024), id_s,
+                    kk > 0);
+        }
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t oa = (kk >> 2) * ATOM + (kk & 3) * 32, ob = (kk >> 2) * QATOM + (kk & 3) * 32;
+          umma_bf16(tmem + COL_DP, sdesc_sw128(sb + OFF_V + oa, 16, 1024), sdesc_sw128(db + ob, 16, 1024), id_s,
+                    kk > 0);
+        }
+        umma_commit(B(B_SF));
+      };
+      mbar_wait(B(B_KV), 0);
+      issue_s(0);
+      for (int k = 0; k < total; ++k) {
+        const int s = k & 1;
+        mbar_wait(B(B_SE), k & 1);
+        if (k + 1 < total) issue_s(k + 1);
+        mbar_wait(B(B_PF), k & 1);
+        tc_fence_after();
+        const uint32_t qb = sb + OFF_Q + s * QTILE, db = sb + OFF_DO + s * QTILE;
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {  // K = 64 rows, 16 per MMA
+          umma_bf16(tmem + COL_DV, sdesc_sw128(sb + OFF_PT + kk * 32, 16, 1024),
+                    sdesc_sw128(db + kk * 2048, QATOM, 1024), id_acc, (k > 0 || kk > 0) ? 1u : 0u);
+        }
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+          umma_bf16(tmem + COL_DK, sdesc_sw128(sb + OFF_DST + kk * 32, 16, 1024),
+                    sdesc_sw128(qb + kk * 2048, QATOM, 1024), id_acc, (k > 0 || kk > 0) ? 1u : 0u);
+        }
+        umma_commit(B(B_QE + s));
+        umma_commit(B(B_PE));
+      }
+    }
+  } else if (warp == 2 || warp == 3) {
+    // row-info loader: lse2 / D / vis of the 64 rows of each Q tile -> smem ring
+    const int r = threadIdx.x - 64;
+    float* info = reinterpret_cast<float*>(smem + OFF_INFO);
+    for (int k = 0; k < total; ++k) {
+      const int s = k & 1;
+      int h, qt;
+      decode_it(k, h, qt);
+      if (k >= 2) mbar_wait(B(B_IE + s), ((k >> 1) - 1) & 1);
+      const size_t ci = (size_t)h * capq + qt * BR + r;
+      info[(s * 3 + 0) * BR + r] = __ldg(lse2c + ci);
+      info[(s * 3 + 1) * BR + r] = __ldg(Dc + ci);
+      reinterpret_cast<int*>(info)[(s * 3 + 2) * BR + r] = __ldg(visc + ci);
+      mbar_arrive(B(B_IF + s));
+    }
+  } else {
+    // softmax-gradient warps: thread j <-> key k0 + j <-> TMEM lane j
+    const int j = threadIdx.x - 128;
+    const int kj = k0 + j;
+    const uint32_t tl = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+    const float sl2 = static_cast<float>(kLog2e / sqrt(static_cast<double>(D)));
+    const float* info = reinterpret_cast<const float*>(smem + OFF_INFO);
+    uint8_t* pt_gen = smem + OFF_PT;
+    uint8_t* dst_gen = smem + OFF_DST;
+    for (int k = 0; k < total; ++k) {
+      const int s = k & 1;
+      mbar_wait(B(B_SF), k & 1);
+      tc_fence_after();
+      uint32_t sv[64], dp[64];
+      __syncwarp();
+      tmem_ld32(tl + COL_S, sv);
+      tmem_ld32(tl + COL_S + 32, sv + 32);
+      tmem_ld32(tl + COL_DP, dp);
+      tmem_ld32(tl + COL_DP + 32, dp + 32);
+      tmem_wait_ld();
+      tc_fence_before();
+      mbar_arrive(B(B_SE));
+      mbar_wait(B(B_IF + s), (k >> 1) & 1);
+      const float* l2 = info + (s * 3 + 0) * BR;
+      const float* dd = info + (s * 3 + 1) * BR;
+      const int* vv = reinterpret_cast<const int*>(info) + (s * 3 + 2) * BR;
+      uint32_t pp[32], pd[32];
+#pragma unroll
+      for (int c = 0; c < 64; c += 2) {
+        const float p0 = (kj < vv[c]) ? fast_exp2(__uint_as_float(sv[c]) * sl2 - l2[c]) : 0.f;
+        const float p1 = (kj < vv[c + 1]) ? fast_exp2(__uint_as_float(sv[c + 1]) * sl2 - l2[c + 1]) : 0.f;
+        pp[c / 2] = pack_bf16x2(p0, p1);
+        pd[c / 2] = pack_bf16x2(p0 * (__uint_as_float(dp[c]) - dd[c]), p1 * (__uint_as_float(dp[c + 1]) - dd[c + 1]));
+      }
+      mbar_arrive(B(B_IE + s));
+      if (k > 0) mbar_wait(B(B_PE), (k - 1) & 1);  // previous dV/dK MMAs done with P^T / dS^T
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        *reinterpret_cast<uint4*>(pt_gen + swz(j, q)) = make_uint4(pp[4 * q], pp[4 * q + 1], pp[4 * q + 2], pp[4 * q + 3]);
+        *reinterpret_cast<uint4*>(dst_gen + swz(j, q)) =
+            make_uint4(pd[4 * q], pd[4 * q + 1], pd[4 * q + 2], pd[4 * q + 3]);
+      }
+      fence_proxy_async_smem();
+      tc_fence_before();
+      mbar_arrive(B(B_PF));
+    }
+    const bool valid = kj < nsel;
+    float4* dvr = reinterpret_cast<float4*>(dV + ((size_t)g * cap + kj) * D);
+    float4* dkr = reinterpret_cast<float4*>(dK + ((size_t)g * cap + kj) * D);
+    if (total > 0) {
+      mbar_wait(B(B_PE), (total - 1) & 1);
+      tc_fence_after();
+      const float scale = static_cast<float>(1.0 / sqrt(static_cast<double>(D)));
+#pragma unroll
+      for (int c4 = 0; c4 < 4; ++c4) {
+        uint32_t a[32], b[32];
+        __syncwarp();
+        tmem_ld32(tl + COL_DV + c4 * 32, a);
+        tmem_ld32(tl + COL_DK + c4 * 32, b);
+        tmem_wait_ld();
+        if (valid) {
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            dvr[c4 * 8 + q] = make_float4(__uint_as_float(a[4 * q]), __uint_as_float(a[4 * q + 1]),
+                                          __uint_as_float(a[4 * q + 2]), __uint_as_float(a[4 * q + 3]));
+            dkr[c4 * 8 + q] = make_float4(__uint_as_float(b[4 * q]) * scale, __uint_as_float(b[4 * q + 1]) * scale,
+                                          __uint_as_float(b[4 * q + 2]) * scale, __uint_as_float(b[4 * q + 3]) * scale);
+          }
+        }
+      }
+    } else if (valid) {
+      for (int q = 0; q < 32; ++q) {
+        dvr[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+        dkr[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    __syncwarp();
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+}  // namespace bwd
+}  // namespace omni
+
+using namespace omni;
+
+int omni_make_tmap_rows(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols_elems, int elem_bytes,
+                        uint32_t box_cols, uint32_t box_rows);
+
+static inline int capq_of(int n) { return ((n + 127) / 128) * 128; }
+
+extern "C" size_t omni_sparse_attn_bwd_workspace(int n_q_heads, int seq_len) {
+  const size_t rows = (size_t)n_q_heads * capq_of(seq_len);
+  return rows * bwd::D * 2 * 2 + rows * 4 * 3 + 1024;
+}
+
+extern "C" int omni_sparse_attn_bwd(const void* Q, const void* K_sel, const void* V_sel, const void* O, const void* dO,
+                                    const float* lse, const int32_t* rows, const int32_t* counts,
+                                    const int32_t* selected, const int32_t* sel_counts, int n_q_heads, int n_kv_heads,
+                                    int seq_len, int head_dim, int cap, float* dQ, float* dK_sel, float* dV_sel,
+                                    float* dV_sink, void* workspace, void* stream) {
+  OMNI_CHECK(head_dim == 128, OMNI_E_SHAPE, "sparse attention backward requires head_dim == 128");
+  OMNI_CHECK(n_kv_heads >= 1 && n_q_heads % n_kv_heads == 0, OMNI_E_SHAPE, "n_q_heads must be a multiple of n_kv_heads");
+  OMNI_CHECK(n_q_heads / n_kv_heads <= 16, OMNI_E_SHAPE, "at most 16 Q heads per KV group");
+  OMNI_CHECK(cap >= 128 && cap % 128 == 0, OMNI_E_SHAPE, "cap must be a positive multiple of 128");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int rep = n_q_heads / n_kv_heads;
+  const int capq = capq_of(seq_len);
+  const size_t crow = (size_t)n_q_heads * capq;
+  uint8_t* ws = static_cast<uint8_t*>(workspace);
+  __nv_bfloat16* Qc = reinterpret_cast<__nv_bfloat16*>(ws);
+  __nv_bfloat16* dOc = Qc + crow * bwd::D;
+  float* lse2c = reinterpret_cast<float*>(dOc + crow * bwd::D);
+  float* Dc = lse2c + crow;
+  int32_t* visc = reinterpret_cast<int32_t*>(Dc + crow);
+  OMNI_CUDA_TRY(cudaMemsetAsync(dQ, 0, sizeof(float) * (size_t)n_q_heads * seq_len * head_dim, st));
+  OMNI_CUDA_TRY(cudaMemsetAsync(dK_sel, 0, sizeof(float) * (size_t)n_kv_heads * cap * head_dim, st));
+  OMNI_CUDA_TRY(cudaMemsetAsync(dV_sel, 0, sizeof(float) * (size_t)n_kv_heads * cap * head_dim, st));
+  OMNI_CUDA_TRY(cudaMemsetAsync(dV_sink, 0, sizeof(float) * (size_t)n_kv_heads * head_dim, st));
+  bwd::bwd_prep_kernel<<<dim3(capq / 8, n_q_heads), 256, 0, st>>>(
+      static_cast<const __nv_bfloat16*>(Q), static_cast<const __nv_bfloat16*>(O),
+      static_cast<const __nv_bfloat16*>(dO), lse, rows, counts, selected, sel_counts, seq_len, rep, capq, Qc, dOc,
+      lse2c, Dc, visc, dV_sink);
+  int rc = omni_launch_check();
+  if (rc) return rc;
+  CUtensorMap tq128, tdo128, tq64, tdo64, tk, tv;
+  if ((rc = omni_make_tmap_rows(&tq128, Qc, crow, 128, 2, 64, 128))) return rc;
+  if ((rc = omni_make_tmap_rows(&tdo128, dOc, crow, 128, 2, 64, 128))) return rc;
+  if ((rc = omni_make_tmap_rows(&tq64, Qc, crow, 128, 2, 64, 64))) return rc;
+  if ((rc = omni_make_tmap_rows(&tdo64, dOc, crow, 128, 2, 64, 64))) return rc;
+  if ((rc = omni_make_tmap_rows(&tk, K_sel, (uint64_t)n_kv_heads * cap, 128, 2, 64, 128))) return rc;
+  if ((rc = omni_make_tmap_rows(&tv, V_sel, (uint64_t)n_kv_heads * cap, 128, 2, 64, 128))) return rc;
+  static bool attr = false;
+  if (!attr) {
+    OMNI_CUDA_TRY(cudaFuncSetAttribute(bwd::dq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bwd::dq::SMEM));
+    OMNI_CUDA_TRY(cudaFuncSetAttribute(bwd::dkv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bwd::dkv::SMEM));
+    attr = true;
+  }
+  const int n_tiles = capq / 128;
+  bwd::dq_kernel<<<n_tiles * n_q_heads, 256, bwd::dq::SMEM, st>>>(tq128, tdo128, tk, tv, rows, counts, lse2c, Dc,
+                                                                    visc, n_q_heads, rep, seq_len, cap, capq, n_tiles,
+                                                                    dQ);
+  if ((rc = omni_launch_check())) return rc;
+  bwd::dkv_kernel<<<dim3(cap / 128, n_kv_heads), 256, bwd::dkv::SMEM, st>>>(tq64, tdo64, tk, tv, rows, counts,
+                                                                            selected, sel_counts, lse2c, Dc, visc, rep,
+                                                                            seq_len, cap, capq, dK_sel, dV_sel);
+  return omni_launch_check();
 }
