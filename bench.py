@@ -55,6 +55,10 @@ def parse():
     return ap.parse_args()
 
 
+def log(msg: str) -> None:
+    print(f"[bench {time.strftime('%H:%M:%S')}] {msg}", file=sys.stderr, flush=True)
+
+
 def peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -410,6 +414,7 @@ def run_ours(args):
                          "active_frac": float(res.active.float().mean())}
     if world == 1:
         line["selection"]["work_ratio_vs_dense_causal"] = flops / (4.0 * D * HQ * n * (n + 1) / 2)
+        log("timed region done; per-kernel breakdown")
         # ----- per-kernel breakdown and the K4 roofline (dominant kernel, own stream events)
         rows, counts, sel = res.rows, res.counts, res.selection
         fa = lambda: ops.sparse_attn_fwd(Q, res.K_sel, res.V_sel, V, rows, counts, sel.selected, sel.counts, 0, O,
@@ -430,6 +435,7 @@ def run_ours(args):
         n_ours, n_all, names = count_launches(step)
         line["gpu_launches"] = n_ours * args.steps
         line["gpu_launches_per_step"] = {"ours": n_ours, "all": n_all, "kernels": names}
+        log("dense FA baselines")
         # ----- dense FA comparators on the same tensors
         if not args.no_dense:
             dense = dense_baselines(Q, K, V, args.steps, 2, args.flashinfer)
@@ -437,6 +443,7 @@ def run_ours(args):
             if "fastest_ms" in dense:
                 line["speedup_vs_dense_fa"] = dense["fastest_ms"] / ms
                 line["dense_fa_tflops"] = dense["dense_causal_flops"] / (dense["fastest_ms"] / 1e3) / 1e12
+        log("knob sweep")
         # ----- second operating point (paper's tau=0.12, p=0.75) and lazier workload
         if not args.no_knobs and not args.no_dense and "fastest_ms" in line.get("dense_fa", {}):
             sweep = []
@@ -453,6 +460,7 @@ def run_ours(args):
                               "work_ratio": work_flops(r2, HKV) / (4.0 * D * HQ * n * (n + 1) / 2)})
                 del Q2, K2, V2, O2, r2
             line["knob_sweep"] = sweep
+        log("e2e")
         # ----- end-to-end through the public API with host buffers
         if not args.no_e2e:
             hQ, hK, hV = (x.cpu().pin_memory() for x in (Q, K, V))
@@ -470,6 +478,7 @@ def run_ours(args):
             line["e2e"] = {"value": n / (e_ms / 1e3), "unit": "tok/s", "ms_per_step": e_ms,
                            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": hO.numel() * hO.element_size(),
                            "api": "pipeline.sparse_prefill_device with pinned host Q/K/V in, O out"}
+        log("cpu baseline")
         # ----- CPU reference path on the host cores (bounded sample)
         if not args.no_cpu:
             try:
@@ -478,6 +487,7 @@ def run_ours(args):
                                         "seconds_per_step_extrapolated": t_step, "sample": desc}
             except Exception as e:  # noqa: BLE001
                 line["cpu_baseline"] = {"error": str(e)[:200]}
+        log("decode section")
         # ----- decode (C5 shape at 1 GPU, sequence-sharded across ranks at N>1)
         if not args.no_decode:
             del res
