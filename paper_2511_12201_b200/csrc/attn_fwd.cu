@@ -9,7 +9,7 @@
 // mask costs one compare per score and the tile loop stops at
 // ceil(vis(last row) / 128) (the causal staircase skips the rest).
 //
-// Warp roles (256 threads, 1 CTA / SM, ~193 KB smem):
+// Warp roles (384 threads, 1 CTA / SM, ~196 KB smem):
 //   warp 0      TMA producer: K_j, V_j tiles (2 x 64-column SW128 boxes each)
 //               into 2-stage K and V rings.
 //   warp 1      TMEM allocator + single-thread tcgen05.mma issuer:
@@ -18,8 +18,8 @@
 //                 O  += P_j V_j  (M=128, N=128, K=128; O in columns [256,384))
 //               issue order QK_j, PV_{j-1} so the tensor core computes the
 //               next scores while the softmax warps work on the current ones.
-//   warps 4-7   softmax / correction / epilogue, thread i <-> row i <-> TMEM
-//               lane i. exp2-domain online softmax with lazy rescaling (the
+//   warps 4-11  softmax / correction / epilogue, two warps per TMEM lane
+//               quarter (one per 64-key half; row max exchanged in smem). exp2-domain online softmax with lazy rescaling (the
 //               O accumulator is corrected only when the running max grows by
 //               more than 2^8), P written bf16 into a 128B-swizzled smem tile
 //               (the A operand of the PV MMA).
@@ -40,7 +40,8 @@ constexpr uint32_t OFF_Q = 0;
 constexpr uint32_t OFF_K = OFF_Q + TILE;       // 2 stages
 constexpr uint32_t OFF_V = OFF_K + 2 * TILE;   // 2 stages
 constexpr uint32_t OFF_P = OFF_V + 2 * TILE;
-constexpr uint32_t OFF_BAR = OFF_P + TILE;
+constexpr uint32_t OFF_XCH = OFF_P + TILE;      // row max / sum exchange [3][2][128] f32
+constexpr uint32_t OFF_BAR = OFF_XCH + 3 * 2 * 128 * 4;
 // barrier slots (8 bytes each)
 enum { B_QFULL = 0, B_KFULL = 1, B_KEMPTY = 3, B_VFULL = 5, B_VEMPTY = 7, B_SFULL = 9, B_SEMPTY = 11,
        B_PFULL = 13, B_PVDONE = 14, B_COUNT = 15 };
@@ -54,7 +55,7 @@ __device__ __forceinline__ uint32_t swz(uint32_t row, uint32_t chunk16) {
   return row * 128u + ((chunk16 ^ (row & 7u)) << 4);
 }
 
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(384, 1)
 sparse_fwd_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
                   const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __restrict__ Vorig,
                   const int32_t* __restrict__ rows, const int32_t* __restrict__ counts,
@@ -89,16 +90,16 @@ sparse_fwd_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constan
     s_nt = (count_le(selg, nsel, last) + BN - 1) / BN;
     tma_prefetch_desc(&tm_k);
     tma_prefetch_desc(&tm_v);
-    mbar_init(B(B_QFULL), 128);
+    mbar_init(B(B_QFULL), 256);
     for (int s = 0; s < 2; ++s) {
       mbar_init(B(B_KFULL + s), 1);
       mbar_init(B(B_KEMPTY + s), 1);
       mbar_init(B(B_VFULL + s), 1);
       mbar_init(B(B_VEMPTY + s), 1);
       mbar_init(B(B_SFULL + s), 1);
-      mbar_init(B(B_SEMPTY + s), 128);
+      mbar_init(B(B_SEMPTY + s), 256);
     }
-    mbar_init(B(B_PFULL), 128);
+    mbar_init(B(B_PFULL), 256);
     mbar_init(B(B_PVDONE), 1);
     fence_mbar_init();
   }
@@ -169,89 +170,100 @@ sparse_fwd_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constan
     }
   } else if (warp >= 4) {
     // ------------------------------------------------------ softmax warps
-    const int i = threadIdx.x - 128;  // row within the tile == TMEM lane
+    // Two warps per TMEM lane quarter: warp w owns rows 32*(w%4) .. +31 and the
+    // key half hf = (w-4)/4 of every tile (columns hf*64 .. +63). The row max is
+    // exchanged between the pair through smem + a 64-thread named barrier.
+    const int q4 = warp & 3, hf = (warp - 4) >> 2;
+    const int i = q4 * 32 + lane;  // row within the tile == TMEM lane
     const bool rvalid = i < nrows;
     const int pos = rvalid ? __ldg(rows_t + i) : 0;
     const int vis = rvalid ? count_le(selg, nsel, pos) : 0;
-    const uint32_t tl = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+    const uint32_t tl = tmem + ((uint32_t)(q4 * 32) << 16);
+    const uint32_t bar_id = 1 + q4;
+    float* xch = reinterpret_cast<float*>(smem + OFF_XCH);  // [2 parity][2 halves][128 rows]
     float m_run = -INFINITY, l_run = 0.f;
     if (nt > 0) {
-      // Q row -> swizzled K-major smem tile (A operand of S = Q K^T).
-      const uint4* qrow = reinterpret_cast<const uint4*>(Q + ((size_t)h * N + pos) * D);
-      uint8_t* q_gen = smem + OFF_Q;
+      // Q row half -> swizzled K-major smem tile (A operand of S = Q K^T).
+      const uint4* qrow = reinterpret_cast<const uint4*>(Q + ((size_t)h * N + pos) * D) + hf * 8;
+      uint8_t* q_gen = smem + OFF_Q + hf * ATOM;
 #pragma unroll
-      for (int c = 0; c < 16; ++c) {
+      for (int c = 0; c < 8; ++c) {
         const uint4 v = rvalid ? __ldg(qrow + c) : make_uint4(0, 0, 0, 0);
-        *reinterpret_cast<uint4*>(q_gen + (c >> 3) * ATOM + swz(i, c & 7)) = v;
+        *reinterpret_cast<uint4*>(q_gen + swz(i, c)) = v;
       }
       fence_proxy_async_smem();
       mbar_arrive(B(B_QFULL));
 
       const float sl2 = static_cast<float>(kLog2e / sqrt(static_cast<double>(D)));
-      uint8_t* p_gen = smem + OFF_P;
+      uint8_t* p_gen = smem + OFF_P + hf * ATOM;
       for (int j = 0; j < nt; ++j) {
         const int sb = j & 1;
         mbar_wait(B(B_SFULL + sb), (j >> 1) & 1);
         tc_fence_after();
-        uint32_t sr[128];
+        uint32_t sr[64];
         __syncwarp();
-        tmem_ld32(tl + sb * BN + 0, sr);
-        tmem_ld32(tl + sb * BN + 32, sr + 32);
-        tmem_ld32(tl + sb * BN + 64, sr + 64);
-        tmem_ld32(tl + sb * BN + 96, sr + 96);
+        tmem_ld32(tl + sb * BN + hf * 64, sr);
+        tmem_ld32(tl + sb * BN + hf * 64 + 32, sr + 32);
         tmem_wait_ld();
         tc_fence_before();
         mbar_arrive(B(B_SEMPTY + sb));
 
-        const int lim = vis - j * BN;
+        // raw-score max over this half (mask only on the staircase boundary)
+        const int lim = vis - j * BN - hf * 64;
+        if (!__all_sync(0xffffffffu, lim >= 64)) {
+#pragma unroll
+          for (int c = 0; c < 64; ++c)
+            if (c >= lim) sr[c] = __float_as_uint(-INFINITY);
+        }
         float mt = -INFINITY;
 #pragma unroll
-        for (int c = 0; c < 128; ++c) {
-          const float x = (c < lim) ? __uint_as_float(sr[c]) * sl2 : -INFINITY;
-          sr[c] = __float_as_uint(x);
-          mt = fmaxf(mt, x);
-        }
-        const float m_new = fmaxf(m_run, mt);
+        for (int c = 0; c < 64; c += 2) mt = fmax3(mt, __uint_as_float(sr[c]), __uint_as_float(sr[c + 1]));
+        xch[((j & 1) * 2 + hf) * 128 + i] = mt;
+        named_bar_sync(bar_id, 64);
+        mt = fmaxf(mt, xch[((j & 1) * 2 + (hf ^ 1)) * 128 + i]);
+        const float m_new = fmaxf(m_run, mt * sl2);
         const bool resc = m_new > m_run + 8.0f;
         float alpha = 1.f;
         if (resc) {
           alpha = (m_run == -INFINITY) ? 0.f : fast_exp2(m_run - m_new);
           m_run = m_new;
         }
-        const float mu = (m_run == -INFINITY) ? 0.f : m_run;
-        float rs = 0.f;
-        uint32_t pk[64];
+        const float nmu = (m_run == -INFINITY) ? 0.f : -m_run;
+        float rs0 = 0.f, rs1 = 0.f;
+        uint32_t pk[32];
 #pragma unroll
-        for (int c = 0; c < 64; ++c) {
-          const float p0 = fast_exp2(__uint_as_float(sr[2 * c]) - mu);
-          const float p1 = fast_exp2(__uint_as_float(sr[2 * c + 1]) - mu);
-          rs += p0 + p1;
-          pk[c] = pack_bf16x2(p0, p1);
+        for (int c = 0; c < 64; c += 2) {
+          const float x0 = fmaf(__uint_as_float(sr[c]), sl2, nmu);
+          const float x1 = fmaf(__uint_as_float(sr[c + 1]), sl2, nmu);
+          // a quarter of the exponentials on the FMA pipe (MUFU relief)
+          const float p0 = ((c & 15) >= 12) ? exp2_poly(x0) : fast_exp2(x0);
+          const float p1 = ((c & 15) >= 12) ? exp2_poly(x1) : fast_exp2(x1);
+          rs0 += p0;
+          rs1 += p1;
+          pk[c >> 1] = pack_bf16x2(p0, p1);
         }
-        l_run = l_run * alpha + rs;
+        l_run = l_run * alpha + (rs0 + rs1);
 
         if (j > 0) {
           mbar_wait(B(B_PVDONE), (j - 1) & 1);  // PV_{j-1} finished: O stable, P buffer free
           tc_fence_after();
           if (__any_sync(0xffffffffu, resc)) {
-            __syncwarp();
 #pragma unroll
-            for (int q4 = 0; q4 < 4; ++q4) {
+            for (int q = 0; q < 2; ++q) {
               uint32_t o[32];
-              tmem_ld32(tl + COL_O + q4 * 32, o);
+              __syncwarp();
+              tmem_ld32(tl + COL_O + hf * 64 + q * 32, o);
               tmem_wait_ld();
 #pragma unroll
               for (int c = 0; c < 32; ++c) o[c] = __float_as_uint(__uint_as_float(o[c]) * alpha);
-              tmem_st32(tl + COL_O + q4 * 32, o);
+              tmem_st32(tl + COL_O + hf * 64 + q * 32, o);
             }
             tmem_wait_st();
           }
         }
 #pragma unroll
-        for (int c = 0; c < 16; ++c) {
-          *reinterpret_cast<uint4*>(p_gen + (c >> 3) * ATOM + swz(i, c & 7)) =
-              make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
-        }
+        for (int c = 0; c < 8; ++c)
+          *reinterpret_cast<uint4*>(p_gen + swz(i, c)) = make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
         fence_proxy_async_smem();
         tc_fence_before();
         mbar_arrive(B(B_PFULL));
@@ -260,31 +272,32 @@ sparse_fwd_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constan
       tc_fence_after();
     }
     // ------------------------------------------------------ epilogue
-    uint32_t o[128];
+    xch[(2 * 2 + hf) * 128 + i] = l_run;  // third slot pair holds the row-sum halves
+    named_bar_sync(bar_id, 64);
+    const float l_tot = l_run + xch[(2 * 2 + (hf ^ 1)) * 128 + i];
+    uint32_t o[64];
     if (nt > 0) {
       __syncwarp();
-      tmem_ld32(tl + COL_O + 0, o);
-      tmem_ld32(tl + COL_O + 32, o + 32);
-      tmem_ld32(tl + COL_O + 64, o + 64);
-      tmem_ld32(tl + COL_O + 96, o + 96);
+      tmem_ld32(tl + COL_O + hf * 64, o);
+      tmem_ld32(tl + COL_O + hf * 64 + 32, o + 32);
       tmem_wait_ld();
     }
     if (rvalid) {
-      uint4* dst = reinterpret_cast<uint4*>(O + ((size_t)h * N + pos) * D);
-      if (l_run > 0.f) {
-        const float inv = 1.f / l_run;
+      uint4* dst = reinterpret_cast<uint4*>(O + ((size_t)h * N + pos) * D) + hf * 8;
+      if (l_tot > 0.f) {
+        const float inv = 1.f / l_tot;
 #pragma unroll
-        for (int c = 0; c < 16; ++c) {
+        for (int c = 0; c < 8; ++c) {
           const float* f = reinterpret_cast<const float*>(o + 8 * c);
           dst[c] = make_uint4(pack_bf16x2(f[0] * inv, f[1] * inv), pack_bf16x2(f[2] * inv, f[3] * inv),
                               pack_bf16x2(f[4] * inv, f[5] * inv), pack_bf16x2(f[6] * inv, f[7] * inv));
         }
-        if (lse) lse[(size_t)h * N + pos] = static_cast<float>(M_LN2) * (m_run + log2f(l_run));
+        if (lse && hf == 0) lse[(size_t)h * N + pos] = static_cast<float>(M_LN2) * (m_run + log2f(l_tot));
       } else {
-        const uint4* src = reinterpret_cast<const uint4*>(Vorig + ((size_t)g * N + sink) * D);
+        const uint4* src = reinterpret_cast<const uint4*>(Vorig + ((size_t)g * N + sink) * D) + hf * 8;
 #pragma unroll
-        for (int c = 0; c < 16; ++c) dst[c] = __ldg(src + c);
-        if (lse) lse[(size_t)h * N + pos] = -INFINITY;
+        for (int c = 0; c < 8; ++c) dst[c] = __ldg(src + c);
+        if (lse && hf == 0) lse[(size_t)h * N + pos] = -INFINITY;
       }
     }
   }
@@ -327,7 +340,7 @@ extern "C" int omni_sparse_attn_fwd(const void* Q, const void* K_sel, const void
   }
   const int n_tiles = (seq_len + fwd::BM - 1) / fwd::BM;
   dim3 grid(n_tiles * n_q_heads);
-  fwd::sparse_fwd_kernel<<<grid, 256, fwd::SMEM_BYTES, static_cast<cudaStream_t>(stream)>>>(
+  fwd::sparse_fwd_kernel<<<grid, 384, fwd::SMEM_BYTES, static_cast<cudaStream_t>(stream)>>>(
       tk, tv, static_cast<const __nv_bfloat16*>(Q), static_cast<const __nv_bfloat16*>(V), rows, counts, selected,
       sel_counts, n_q_heads, n_q_heads / n_kv_heads, seq_len, cap, seq_len, sink_index, n_tiles,
       static_cast<__nv_bfloat16*>(O), lse);

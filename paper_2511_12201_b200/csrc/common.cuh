@@ -216,6 +216,31 @@ __device__ __forceinline__ float fast_exp2(float x) {
   return y;
 }
 
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+
+// 2^x on the FMA/ALU pipes (no MUFU): round-to-nearest split x = n + f,
+// f in [-0.5, 0.5], degree-3 relative-minimax polynomial (max rel err 7.5e-5,
+// below the bf16 rounding P receives). Valid for x <= 127; -inf -> 0.
+__device__ __forceinline__ float exp2_poly(float x) {
+  const bool zero = x < -126.f;  // masked (-inf) and underflowing entries are exactly 0
+  x = fmaxf(x, -126.f);
+  const float r = x + 12582912.f;  // 1.5 * 2^23: integer part lands in the low mantissa bits
+  const float f = x - (r - 12582912.f);
+  float p = fmaf(0.05517165f, f, 0.24261116f);
+  p = fmaf(p, f, 0.69326099f);
+  p = fmaf(p, f, 0.99992807f);
+  const float v = __int_as_float(__float_as_int(p) + ((__float_as_int(r) - 0x4B400000) << 23));
+  return zero ? 0.f : v;
+}
+
+__device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
 // Number of entries of ascending `a[0..n)` that are <= key (upper bound).
 __device__ __forceinline__ int count_le(const int32_t* __restrict__ a, int n, int key) {
   int lo = 0, hi = n;
