@@ -1,15 +1,24 @@
-// K7: slimmed decode attention (split-K flash decoding over the slim cache).
+// K7: slimmed decode attention over the slim cache (split-K flash decoding).
 //
 // Replaces classify_decode_query + _fetched_segments + decode_attention
-// (decode.py:124-194) for a batch of sequences under GQA rule B. Work unit =
-// (sequence, KV group, 256-key chunk) so 32 sequences x 4 groups x ~120
-// chunks fill the 148 SMs many times over. Every CTA re-derives its group's
-// lazy/active flags in float64 from the frozen probe keys (7 x 2 dot products
-// — cheaper than a separate launch); a vision chunk of a group whose Q heads
-// are all lazy exits before touching HBM, which is exactly the KV-fetch skip
-// of decode.py:176-190. The kernel is HBM-bound: K and V of a chunk are read
-// once into padded shared memory and reused by all Q heads of the group.
-// A second kernel merges the per-chunk (max, sum, acc) partials per Q head.
+// (decode.py:124-194) for a batch of sequences under GQA rule B.
+//
+//   decode_flags_kernel   one warp per (sequence, Q head): float64
+//                         two-logit classification against the frozen probe
+//                         keys (query_select.py:63-68), head 0 forced active.
+//   decode_partial_kernel CTA = (2048-key chunk, KV group, sequence), 4 warps x
+//                         512 keys. A group's key list is [vision (only if any
+//                         of its Q heads is active — the fetch skip of
+//                         decode.py:176-190), text, answer]; lazy Q heads see
+//                         -inf on vision keys (exclusion, decode.py:12-16).
+//                         The group's <= 16 Q heads form the M=16 rows of
+//                         mma.sync.m16n8k16 tiles, so each K / V row is read
+//                         from HBM exactly once and feeds every head. Head-dim
+//                         and key orders inside a tile are permuted so every
+//                         lane issues contiguous 16-byte loads straight into
+//                         MMA fragments (no shared-memory staging).
+//   decode_combine_kernel merges the per-chunk (max, sum, acc) partials.
+// HBM-bound: bytes = fetched vision + text + answer K/V rows, once each.
 #include <math.h>
 
 #include "common.cuh"
@@ -17,207 +26,230 @@
 namespace omni {
 namespace dec {
 
-constexpr int CHUNK = 256;
 constexpr int D = 128;
-constexpr int ROWB = D * 2 + 16;  // padded smem row (bytes): conflict-free 16B reads
-constexpr int MAXREP = 16;
+constexpr int WARP_KEYS = 512;
+constexpr int CTA_KEYS = 4 * WARP_KEYS;
+constexpr int MAXREP = 8;  // rows of the m16 tile used (rows 8..15 stay zero)
 
-__global__ void __launch_bounds__(256) decode_partial_kernel(
-    const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ vk, const __nv_bfloat16* __restrict__ vv,
-    const int32_t* __restrict__ vlen, const __nv_bfloat16* __restrict__ tk, const __nv_bfloat16* __restrict__ tv,
-    int nt, const __nv_bfloat16* __restrict__ ak, const __nv_bfloat16* __restrict__ av, int na,
-    const double* __restrict__ k_lazy, const double* __restrict__ k_act, int Hq, int Hkv, int vcap, int acap,
-    double tau, int preserve, const uint8_t* __restrict__ flags_override, uint8_t* __restrict__ flags_out,
-    int vis_chunks, float* __restrict__ part_ml, float* __restrict__ part_acc, int n_chunks) {
-  extern __shared__ __align__(16) uint8_t sh[];
-  uint8_t* sK = sh;                                   // [CHUNK][ROWB]
-  uint8_t* sV = sh + CHUNK * ROWB;                    // [CHUNK][ROWB]
-  float* sQ = reinterpret_cast<float*>(sh + 2 * CHUNK * ROWB);  // [rep][D]
-  float* sP = sQ + MAXREP * D;                        // [rep][CHUNK]
-  float* sRed = sP + MAXREP * CHUNK;                  // [8][rep] / [4][rep][D] reuse
-  __shared__ int s_flag[MAXREP];
-  __shared__ int s_any;
+__device__ __forceinline__ void mma_bf16_16816(float* c, const uint32_t* a, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
 
-  const int c = blockIdx.x, g = blockIdx.y, s = blockIdx.z;
-  const int rep = Hq / Hkv;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-
-  // ---- flags for this group's Q heads (f64, query_select.py:63-68)
-  if (warp == 0) {
-    const double scale = 1.0 / sqrt(static_cast<double>(D));
-    for (int r = 0; r < rep; ++r) {
-      const int h = g * rep + r;
-      int f;
-      if (flags_override) {
-        f = flags_override[(size_t)s * Hq + h] ? 1 : 0;
-      } else {
-        double dl = 0.0, da = 0.0;
-        for (int e = lane; e < D; e += 32) {
-          const double x = static_cast<double>(__bfloat162float(q[((size_t)s * Hq + h) * D + e]));
-          dl = fma(x, k_lazy[((size_t)s * Hkv + g) * D + e], dl);
-          da = fma(x, k_act[((size_t)s * Hkv + g) * D + e], da);
-        }
-        dl = warp_sum(dl);
-        da = warp_sum(da);
-        const double l0 = dl * scale, l1 = da * scale, mx = fmax(l0, l1);
-        const double e0 = exp(l0 - mx), e1 = exp(l1 - mx);
-        f = (e1 / (e0 + e1) > tau) ? 1 : 0;
-        if (preserve && h == 0) f = 1;
-      }
-      if (lane == 0) {
-        s_flag[r] = f;
-        if (c == 0) flags_out[(size_t)s * Hq + h] = static_cast<uint8_t>(f);
-      }
-    }
-    if (lane == 0) {
-      int any = 0;
-      for (int r = 0; r < rep; ++r) any |= s_flag[r];
-      s_any = any;
-    }
-  }
-  __syncthreads();
-
-  // ---- key range of this chunk
-  const bool is_vis = c < vis_chunks;
-  int k0, k1;
-  const __nv_bfloat16 *kbase = nullptr, *vbase = nullptr;
-  if (is_vis) {
-    const int vl = vlen[s];
-    k0 = c * CHUNK;
-    k1 = min(vl, k0 + CHUNK);
-    if (!s_any) k1 = k0;  // group lazy: no vision fetch
-    kbase = vk + ((size_t)s * Hkv + g) * vcap * D;
-    vbase = vv + ((size_t)s * Hkv + g) * vcap * D;
-  } else {
-    k0 = (c - vis_chunks) * CHUNK;
-    k1 = min(nt + na, k0 + CHUNK);
-  }
-  const int nk = max(0, k1 - k0);
-  float* ml = part_ml + (((size_t)s * Hq + g * rep) * n_chunks + c) * 2;
-  float* acc_out = part_acc + (((size_t)s * Hq + g * rep) * n_chunks + c) * D;
-  if (nk == 0) {
-    if (tid < rep) {
-      ml[(size_t)tid * n_chunks * 2 + 0] = -INFINITY;
-      ml[(size_t)tid * n_chunks * 2 + 1] = 0.f;
-    }
+__global__ void decode_flags_kernel(const __nv_bfloat16* __restrict__ q, const double* __restrict__ k_lazy,
+                                    const double* __restrict__ k_act, int Hq, int Hkv, double tau, int preserve,
+                                    const uint8_t* __restrict__ flags_override, uint8_t* __restrict__ flags) {
+  const int h = blockIdx.x, s = blockIdx.y, lane = threadIdx.x;
+  const int g = h / (Hq / Hkv);
+  if (flags_override) {
+    if (lane == 0) flags[(size_t)s * Hq + h] = flags_override[(size_t)s * Hq + h] ? 1 : 0;
     return;
   }
-
-  // ---- stage q (f32) and the K/V chunk (bf16) in smem
-  for (int e = tid; e < rep * D; e += blockDim.x)
-    sQ[e] = __bfloat162float(q[((size_t)s * Hq + g * rep) * D + e]);
-  for (int e = tid; e < nk * 16; e += blockDim.x) {
-    const int r = e >> 4, cc = e & 15;
-    const int key = k0 + r;
-    const uint4* ks;
-    const uint4* vs;
-    if (is_vis) {
-      ks = reinterpret_cast<const uint4*>(kbase + (size_t)key * D);
-      vs = reinterpret_cast<const uint4*>(vbase + (size_t)key * D);
-    } else if (key < nt) {
-      ks = reinterpret_cast<const uint4*>(tk + (((size_t)s * Hkv + g) * nt + key) * D);
-      vs = reinterpret_cast<const uint4*>(tv + (((size_t)s * Hkv + g) * nt + key) * D);
-    } else {
-      ks = reinterpret_cast<const uint4*>(ak + (((size_t)s * Hkv + g) * acap + (key - nt)) * D);
-      vs = reinterpret_cast<const uint4*>(av + (((size_t)s * Hkv + g) * acap + (key - nt)) * D);
-    }
-    *reinterpret_cast<uint4*>(sK + r * ROWB + cc * 16) = __ldg(ks + cc);
-    *reinterpret_cast<uint4*>(sV + r * ROWB + cc * 16) = __ldg(vs + cc);
+  double dl = 0.0, da = 0.0;
+  for (int e = lane; e < D; e += 32) {
+    const double x = static_cast<double>(__bfloat162float(q[((size_t)s * Hq + h) * D + e]));
+    dl = fma(x, k_lazy[((size_t)s * Hkv + g) * D + e], dl);
+    da = fma(x, k_act[((size_t)s * Hkv + g) * D + e], da);
   }
-  __syncthreads();
+  dl = warp_sum(dl);
+  da = warp_sum(da);
+  if (lane == 0) {
+    const double scale = 1.0 / sqrt(static_cast<double>(D));
+    const double l0 = dl * scale, l1 = da * scale, mx = fmax(l0, l1);
+    const double e0 = exp(l0 - mx), e1 = exp(l1 - mx);
+    int f = (e1 / (e0 + e1) > tau) ? 1 : 0;
+    if (preserve && h == 0) f = 1;
+    flags[(size_t)s * Hq + h] = static_cast<uint8_t>(f);
+  }
+}
 
-  // ---- scores: thread t <-> key t, all Q heads of the group
+__global__ void __launch_bounds__(128) decode_partial_kernel(
+    const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ vk, const __nv_bfloat16* __restrict__ vv,
+    const int32_t* __restrict__ vlen, const __nv_bfloat16* __restrict__ tk, const __nv_bfloat16* __restrict__ tv,
+    int nt, const __nv_bfloat16* __restrict__ ak, const __nv_bfloat16* __restrict__ av, int na, int Hq, int Hkv,
+    int vcap, int acap, const uint8_t* __restrict__ flags, float* __restrict__ part_ml, float* __restrict__ part_acc,
+    int n_chunks) {
+  __shared__ float s_ml[4][MAXREP][2];
+  __shared__ float s_acc[4][MAXREP][D];
+  const int c = blockIdx.x, g = blockIdx.y, s = blockIdx.z;
+  const int rep = Hq / Hkv;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r4 = lane & 3, gid = lane >> 2;  // thread-in-group, group id (row / key / column index)
+
+  // per-row (Q head) vision visibility; row gid (< rep) is this thread's A/C row
+  int any = 0;
+  for (int r = 0; r < rep; ++r) any |= flags[(size_t)s * Hq + g * rep + r];
+  const bool row_valid = gid < rep;
+  const bool row_vis = row_valid && flags[(size_t)s * Hq + g * rep + (row_valid ? gid : 0)];
+  const int vl = vlen[s];
+  const int k_start = any ? 0 : vl;       // skip the vision segment when every head is lazy
+  const int k_end = vl + nt + na;
+  const int w0 = k_start + c * CTA_KEYS + warp * WARP_KEYS;
+  const int w1 = min(k_end, w0 + WARP_KEYS);
+
+  // Q A-fragments with the head-dim permutation: lane r4 owns dims r4*32 .. +31;
+  // k-step ks uses dims r4*32 + ks*4 + {0,1} (a0a1) and {2,3} (a4a5).
+  uint32_t qa[8][4];
+  {
+    uint4 qv[4];
+    const uint4* qrow = reinterpret_cast<const uint4*>(q + ((size_t)s * Hq + g * rep + (row_valid ? gid : 0)) * D) + r4 * 4;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) qv[i] = row_valid ? __ldg(qrow + i) : make_uint4(0, 0, 0, 0);
+    const uint32_t* qw = reinterpret_cast<const uint32_t*>(qv);
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks) {
+      qa[ks][0] = qw[2 * ks];      // row gid, dims +0,+1
+      qa[ks][1] = 0u;              // row gid+8 (padding)
+      qa[ks][2] = qw[2 * ks + 1];  // row gid, dims +2,+3
+      qa[ks][3] = 0u;
+    }
+  }
   const float sl2 = static_cast<float>(kLog2e / sqrt(static_cast<double>(D)));
-  float sc[MAXREP];
+  float m_run = -INFINITY, l_run = 0.f;
+  float acc[16][4];
 #pragma unroll
-  for (int r = 0; r < MAXREP; ++r) sc[r] = 0.f;
-  if (tid < nk) {
-    for (int cc = 0; cc < 16; ++cc) {
-      const uint4 u = *reinterpret_cast<const uint4*>(sK + tid * ROWB + cc * 16);
-      const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
-      float kf[8];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const float2 f = __bfloat1622float2(h2[i]);
-        kf[2 * i] = f.x;
-        kf[2 * i + 1] = f.y;
-      }
-#pragma unroll
-      for (int r = 0; r < MAXREP; ++r) {
-        if (r < rep) {
-          const float4 qa = *reinterpret_cast<const float4*>(sQ + r * D + cc * 8);
-          const float4 qb = *reinterpret_cast<const float4*>(sQ + r * D + cc * 8 + 4);
-          sc[r] += qa.x * kf[0] + qa.y * kf[1] + qa.z * kf[2] + qa.w * kf[3] + qb.x * kf[4] + qb.y * kf[5] +
-                   qb.z * kf[6] + qb.w * kf[7];
-        }
-      }
-    }
-  }
-  // ---- per-head chunk max and exp (exclusion: lazy heads get no vision keys)
-  float mx[MAXREP];
-#pragma unroll
-  for (int r = 0; r < MAXREP; ++r) {
-    float x = -INFINITY;
-    if (r < rep && tid < nk && (!is_vis || s_flag[r])) x = sc[r] * sl2;
-    sc[r] = x;
-    float m = x;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-    mx[r] = m;
-  }
-  if (lane == 0)
-    for (int r = 0; r < rep; ++r) sRed[warp * MAXREP + r] = mx[r];
-  __syncthreads();
-  for (int r = 0; r < rep; ++r) {
-    float m = -INFINITY;
-    for (int w = 0; w < 8; ++w) m = fmaxf(m, sRed[w * MAXREP + r]);
-    mx[r] = m;
-  }
-  __syncthreads();
-  float ls[MAXREP];
-  for (int r = 0; r < rep; ++r) {
-    const float p = (mx[r] == -INFINITY || sc[r] == -INFINITY) ? 0.f : fast_exp2(sc[r] - mx[r]);
-    sP[r * CHUNK + tid] = p;
-    ls[r] = warp_sum(p);
-  }
-  if (lane == 0)
-    for (int r = 0; r < rep; ++r) sRed[warp * MAXREP + r] = ls[r];
-  __syncthreads();
-  if (tid < rep) {
-    float l = 0.f;
-    for (int w = 0; w < 8; ++w) l += sRed[w * MAXREP + tid];
-    ml[(size_t)tid * n_chunks * 2 + 0] = mx[tid];
-    ml[(size_t)tid * n_chunks * 2 + 1] = l;
-  }
-  __syncthreads();
+  for (int i = 0; i < 16; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
 
-  // ---- acc[r][col] = sum_t p[r][t] V[t][col]; thread = (column pair, key quarter)
-  const int cp = tid & 63, kq = tid >> 6;
-  float a0[MAXREP], a1[MAXREP];
+  const size_t sg = (size_t)s * Hkv + g;
+  auto krow = [&](int v) -> const uint4* {
+    const __nv_bfloat16* p;
+    if (v < vl) p = vk + (sg * vcap + v) * D;
+    else if (v < vl + nt) p = tk + (sg * nt + (v - vl)) * D;
+    else p = ak + (sg * acap + (v - vl - nt)) * D;
+    return reinterpret_cast<const uint4*>(p);
+  };
+  auto vrow = [&](int v) -> const uint4* {
+    const __nv_bfloat16* p;
+    if (v < vl) p = vv + (sg * vcap + v) * D;
+    else if (v < vl + nt) p = tv + (sg * nt + (v - vl)) * D;
+    else p = av + (sg * acap + (v - vl - nt)) * D;
+    return reinterpret_cast<const uint4*>(p);
+  };
+
+  for (int kb = w0; kb < w1; kb += 16) {
+    // ---- K fragments: n-tile t covers keys kb + 8t + gid; lane loads dims r4*32 .. +31
+    uint4 kf[2][4];
+    bool kvalid[2];
 #pragma unroll
-  for (int r = 0; r < MAXREP; ++r) a0[r] = a1[r] = 0.f;
-  for (int t = kq * 64; t < min(nk, kq * 64 + 64); ++t) {
-    const float2 v = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(sV + t * ROWB + cp * 4));
+    for (int t = 0; t < 2; ++t) {
+      const int key = kb + 8 * t + gid;
+      kvalid[t] = key < w1;
+      const uint4* p = krow(kvalid[t] ? key : kb) + r4 * 4;
 #pragma unroll
-    for (int r = 0; r < MAXREP; ++r) {
-      if (r < rep) {
-        const float p = sP[r * CHUNK + t];
-        a0[r] = fmaf(p, v.x, a0[r]);
-        a1[r] = fmaf(p, v.y, a1[r]);
+      for (int i = 0; i < 4; ++i) kf[t][i] = __ldg(p + i);
+    }
+    // ---- V rows for the B fragments of P V: keys kb + 2*r4 + {0,1,8,9}, dims gid*16 .. +15
+    uint4 vf[4][2];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int key = kb + 2 * r4 + (u & 1) + 8 * (u >> 1);
+      const uint4* p = vrow(key < w1 ? key : kb) + gid * 2;
+      vf[u][0] = __ldg(p);
+      vf[u][1] = __ldg(p + 1);
+    }
+    // ---- S = Q K^T (rows = heads, cols = 16 keys)
+    float sc[2][4];
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      sc[t][0] = sc[t][1] = sc[t][2] = sc[t][3] = 0.f;
+      const uint32_t* kw = reinterpret_cast<const uint32_t*>(kf[t]);
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks) mma_bf16_16816(sc[t], qa[ks], kw[2 * ks], kw[2 * ks + 1]);
+    }
+    // ---- mask (keys beyond the range; vision keys for lazy heads) and online softmax
+    float x[4];
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int key = kb + 8 * t + 2 * r4 + e;  // C fragment column of this thread
+        const bool ok = row_valid && key < w1 && (key >= vl || row_vis);
+        x[2 * t + e] = ok ? sc[t][e] * sl2 : -INFINITY;
       }
     }
+    float mt = fmaxf(fmaxf(x[0], x[1]), fmaxf(x[2], x[3]));
+    mt = fmaxf(mt, __shfl_xor_sync(0xffffffffu, mt, 1));
+    mt = fmaxf(mt, __shfl_xor_sync(0xffffffffu, mt, 2));
+    const float m_new = fmaxf(m_run, mt);
+    if (m_new > m_run + 8.0f) {  // lazy rescale of this row's accumulator
+      const float alpha = (m_run == -INFINITY) ? 0.f : fast_exp2(m_run - m_new);
+      l_run *= alpha;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        acc[i][0] *= alpha;
+        acc[i][1] *= alpha;
+      }
+      m_run = m_new;
+    }
+    const float mu = (m_run == -INFINITY) ? 0.f : m_run;
+    float p[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      p[e] = fast_exp2(x[e] - mu);
+      l_run += p[e];
+    }
+    // P as the A fragment: a0a1 = keys 2r4,+1 (n-tile 0), a4a5 = keys 8+2r4,+1 (n-tile 1)
+    uint32_t pa[4] = {pack_bf16x2(p[0], p[1]), 0u, pack_bf16x2(p[2], p[3]), 0u};
+    // ---- O += P V over 16 d n-tiles; n-tile nt, column gid <-> dim gid*16 + nt
+#pragma unroll
+    for (int ntl = 0; ntl < 16; ++ntl) {
+      const int w = ntl >> 1, hi = ntl & 1;
+      const uint32_t* v0 = reinterpret_cast<const uint32_t*>(&vf[0][w >> 2]);
+      const uint32_t* v1 = reinterpret_cast<const uint32_t*>(&vf[1][w >> 2]);
+      const uint32_t* v2 = reinterpret_cast<const uint32_t*>(&vf[2][w >> 2]);
+      const uint32_t* v3 = reinterpret_cast<const uint32_t*>(&vf[3][w >> 2]);
+      const int wi = w & 3;
+      const uint32_t sel = hi ? 0x7632u : 0x5410u;
+      const uint32_t b0 = __byte_perm(v0[wi], v1[wi], sel);
+      const uint32_t b1 = __byte_perm(v2[wi], v3[wi], sel);
+      float* cc = acc[ntl];
+      asm volatile(
+          "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+          "{%0,%1,%2,%3};"
+          : "+f"(cc[0]), "+f"(cc[1]), "+f"(cc[2]), "+f"(cc[3])
+          : "r"(pa[0]), "r"(pa[1]), "r"(pa[2]), "r"(pa[3]), "r"(b0), "r"(b1));
+    }
   }
-  float* red = reinterpret_cast<float*>(sK);  // reuse: [4][rep][D]
-  for (int r = 0; r < rep; ++r) {
-    red[(kq * rep + r) * D + 2 * cp] = a0[r];
-    red[(kq * rep + r) * D + 2 * cp + 1] = a1[r];
+  // ---- per-warp row results -> smem; row gid's l is spread over the 4 lanes of its group
+  l_run += __shfl_xor_sync(0xffffffffu, l_run, 1);
+  l_run += __shfl_xor_sync(0xffffffffu, l_run, 2);
+  if (row_valid) {
+    if (r4 == 0) {
+      s_ml[warp][gid][0] = m_run;
+      s_ml[warp][gid][1] = l_run;
+    }
+    // C fragment: acc[nt][0/1] = O[row gid][n = 2*r4 + {0,1}] -> dim n*16 + nt
+#pragma unroll
+    for (int ntl = 0; ntl < 16; ++ntl) {
+      s_acc[warp][gid][(2 * r4) * 16 + ntl] = acc[ntl][0];
+      s_acc[warp][gid][(2 * r4 + 1) * 16 + ntl] = acc[ntl][1];
+    }
   }
   __syncthreads();
-  for (int e = tid; e < rep * D; e += blockDim.x) {
+  // ---- combine the 4 warps, write this chunk's partial per Q head
+  for (int e = threadIdx.x; e < rep * D; e += blockDim.x) {
     const int r = e / D, col = e % D;
-    const float v = red[(0 * rep + r) * D + col] + red[(1 * rep + r) * D + col] + red[(2 * rep + r) * D + col] +
-                    red[(3 * rep + r) * D + col];
-    acc_out[(size_t)r * n_chunks * D + col] = v;
+    float M = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < 4; ++w) M = fmaxf(M, s_ml[w][r][0]);
+    float L = 0.f, o = 0.f;
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      const float m = s_ml[w][r][0];
+      if (m == -INFINITY) continue;
+      const float wt = fast_exp2(m - M);
+      L += wt * s_ml[w][r][1];
+      o += wt * s_acc[w][r][col];
+    }
+    const size_t base = ((size_t)s * Hq + g * rep + r) * n_chunks + c;
+    part_acc[base * D + col] = o;
+    if (col == 0) {
+      part_ml[base * 2 + 0] = M;
+      part_ml[base * 2 + 1] = L;
+    }
   }
 }
 
@@ -251,14 +283,12 @@ __global__ void decode_combine_kernel(const float* __restrict__ part_ml, const f
 
 using namespace omni;
 
-static int dec_chunks(int vcap, int n_text, int n_answer, int* vis_chunks) {
-  *vis_chunks = (vcap + dec::CHUNK - 1) / dec::CHUNK;
-  return *vis_chunks + (n_text + n_answer + dec::CHUNK - 1) / dec::CHUNK;
+static int dec_chunks(int vcap, int n_text, int n_answer) {
+  return (vcap + n_text + n_answer + dec::CTA_KEYS - 1) / dec::CTA_KEYS;
 }
 
 extern "C" size_t omni_decode_workspace(int batch, int n_q_heads, int vcap, int n_text, int acap, int head_dim) {
-  int vc;
-  const int nc = dec_chunks(vcap, n_text, acap, &vc);
+  const int nc = dec_chunks(vcap, n_text, acap);
   return sizeof(float) * (size_t)batch * n_q_heads * nc * (head_dim + 2) + 16;
 }
 
@@ -270,34 +300,25 @@ extern "C" int omni_decode_step(const void* q, const void* vision_k, const void*
                                 void* workspace, void* stream) {
   OMNI_CHECK(head_dim == dec::D, OMNI_E_SHAPE, "decode kernel requires head_dim == 128");
   OMNI_CHECK(n_kv_heads >= 1 && n_q_heads % n_kv_heads == 0, OMNI_E_SHAPE, "n_q_heads must be a multiple of n_kv_heads");
-  OMNI_CHECK(n_q_heads / n_kv_heads <= dec::MAXREP, OMNI_E_SHAPE, "at most 16 Q heads per KV group");
+  OMNI_CHECK(n_q_heads / n_kv_heads <= dec::MAXREP, OMNI_E_SHAPE, "at most 8 Q heads per KV group");
   OMNI_CHECK(tau >= 0.0 && tau < 1.0, OMNI_E_PARAM, "tau must be in [0, 1)");
   OMNI_CHECK(n_answer >= 0 && n_answer <= acap && n_text >= 0, OMNI_E_SHAPE, "answer segment overflow");
   OMNI_CHECK(batch >= 1, OMNI_E_SHAPE, "empty batch");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  int vc;
-  const int nc = dec_chunks(vcap, n_text, n_answer, &vc);
-  const int ncap = dec_chunks(vcap, n_text, acap, &vc);
-  (void)ncap;
+  const int nc = dec_chunks(vcap, n_text, n_answer);
   float* part_ml = static_cast<float*>(workspace);
   float* part_acc = part_ml + (size_t)batch * n_q_heads * nc * 2;
   int* degenerate = reinterpret_cast<int*>(part_acc + (size_t)batch * n_q_heads * nc * head_dim);
   OMNI_CUDA_TRY(cudaMemsetAsync(degenerate, 0, sizeof(int), st));
-  const size_t shm = 2 * dec::CHUNK * dec::ROWB + sizeof(float) * (dec::MAXREP * dec::D + dec::MAXREP * dec::CHUNK +
-                                                                    8 * dec::MAXREP);
-  static bool attr = false;
-  if (!attr) {
-    OMNI_CUDA_TRY(cudaFuncSetAttribute(dec::decode_partial_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)shm));
-    attr = true;
-  }
-  dim3 grid(nc, n_kv_heads, batch);
-  dec::decode_partial_kernel<<<grid, 256, shm, st>>>(
+  dec::decode_flags_kernel<<<dim3(n_q_heads, batch), 32, 0, st>>>(static_cast<const __nv_bfloat16*>(q), k_lazy, k_act,
+                                                                   n_q_heads, n_kv_heads, tau, preserve_first_head,
+                                                                   flags_override, flags);
+  dec::decode_partial_kernel<<<dim3(nc, n_kv_heads, batch), 128, 0, st>>>(
       static_cast<const __nv_bfloat16*>(q), static_cast<const __nv_bfloat16*>(vision_k),
       static_cast<const __nv_bfloat16*>(vision_v), vision_len, static_cast<const __nv_bfloat16*>(text_k),
       static_cast<const __nv_bfloat16*>(text_v), n_text, static_cast<const __nv_bfloat16*>(answer_k),
-      static_cast<const __nv_bfloat16*>(answer_v), n_answer, k_lazy, k_act, n_q_heads, n_kv_heads, vcap, acap, tau,
-      preserve_first_head, flags_override, flags, vc, part_ml, part_acc, nc);
+      static_cast<const __nv_bfloat16*>(answer_v), n_answer, n_q_heads, n_kv_heads, vcap, acap, flags, part_ml,
+      part_acc, nc);
   dec::decode_combine_kernel<<<dim3(n_q_heads, batch), dec::D, 0, st>>>(part_ml, part_acc, nc, out, degenerate);
   int st_code = omni_launch_check();
   if (st_code) return st_code;
