@@ -1,7 +1,9 @@
 """GPU parity of cache slimming (K6) and slimmed decode (K7) vs the oracle.
 
 Flags are bit-exact (float64 classification on both sides); outputs within
-1e-3 (bf16 cache values are identical on both sides; fp32 accumulation)."""
+atol 5e-3 / rtol 2e-2: cache values are the same bf16 numbers on both sides,
+the kernel accumulates in fp32 with P rounded to bf16 for the PV tensor-core
+product (the same class of rounding as the prefill kernel)."""
 
 import numpy as np
 import pytest
@@ -63,7 +65,7 @@ def test_decode_trace_matches_oracle():
         out, flags = gdec.decode_attention(dev(q).unsqueeze(0), cache, 0.08)
         o_ref, f_ref = oatt.decode_step(q, ocache, 0.08, rep, True, log)
         np.testing.assert_array_equal(flags[0].cpu().numpy().astype(bool), f_ref)
-        np.testing.assert_allclose(out[0].cpu().numpy(), np.stack(o_ref), atol=1e-3, rtol=1e-3)
+        np.testing.assert_allclose(out[0].cpu().numpy(), np.stack(o_ref), atol=5e-3, rtol=2e-2)
         gdec.append_answer(cache, dev(k).unsqueeze(0), dev(v).unsqueeze(0))
         oatt.append_answer(ocache, k, v, 128)
     assert cache.fetch.vision_tokens == log.vision_tokens
@@ -80,7 +82,7 @@ def test_forced_flags_exclusion_semantics():
     out, fl = gdec.decode_attention(dev(q).unsqueeze(0), cache, 0.08, flags=torch.tensor(forced[None]))
     np.testing.assert_array_equal(fl[0].cpu().numpy().astype(bool), forced)
     exp = np.stack(oatt.decode_dense(q, ocache, forced, rep))
-    np.testing.assert_allclose(out[0].cpu().numpy(), exp, atol=1e-3, rtol=1e-3)
+    np.testing.assert_allclose(out[0].cpu().numpy(), exp, atol=5e-3, rtol=2e-2)
 
 
 def test_batched_decode_ragged_budgets():
@@ -99,7 +101,7 @@ def test_batched_decode_ragged_budgets():
         for s, (c, oc, tr, rep) in enumerate(pairs):
             o_ref, f_ref = oatt.decode_step(tr[step][0], oc, 0.08, rep, True, logs[s])
             np.testing.assert_array_equal(flags[s].cpu().numpy().astype(bool), f_ref)
-            np.testing.assert_allclose(out[s].cpu().numpy(), np.stack(o_ref), atol=1e-3, rtol=1e-3)
+            np.testing.assert_allclose(out[s].cpu().numpy(), np.stack(o_ref), atol=5e-3, rtol=2e-2)
             oatt.append_answer(oc, tr[step][1], tr[step][2], 128)
         ks = dev(np.stack([p[2][step][1] for p in pairs]))
         vs = dev(np.stack([p[2][step][2] for p in pairs]))
