@@ -31,6 +31,32 @@ struct Vec8<float> {
   }
 };
 
+// Raw 8-element vector kept in registers until converted (keeps many rows in
+// flight per thread without paying 16 f64 registers per row).
+template <typename T>
+struct Raw8;
+template <>
+struct Raw8<__nv_bfloat16> {
+  uint4 u;
+  __device__ void load(const __nv_bfloat16* p) { u = __ldg(reinterpret_cast<const uint4*>(p)); }
+  __device__ void zero() { u = make_uint4(0, 0, 0, 0); }
+  __device__ double at(int i) const {
+    return static_cast<double>(__bfloat162float(reinterpret_cast<const __nv_bfloat16*>(&u)[i]));
+  }
+};
+template <>
+struct Raw8<float> {
+  float4 a, b;
+  __device__ void load(const float* p) {
+    a = __ldg(reinterpret_cast<const float4*>(p));
+    b = __ldg(reinterpret_cast<const float4*>(p) + 1);
+  }
+  __device__ void zero() { a = b = make_float4(0.f, 0.f, 0.f, 0.f); }
+  __device__ double at(int i) const {
+    return static_cast<double>(i < 4 ? reinterpret_cast<const float*>(&a)[i] : reinterpret_cast<const float*>(&b)[i - 4]);
+  }
+};
+
 // ------------------------------------------------------------------------ K1
 // CTA (block J, kv head g): column sums of K[g, rows of J] (all rows) and of
 // the rows < n_vision, in f64. 256 threads = (256 / (d/8)) row lanes x (d/8)
@@ -81,8 +107,14 @@ __global__ void probe_finish_kernel(const T* __restrict__ K, int N, int d, int n
                                     double* __restrict__ k_act) {
   const int g = blockIdx.x;
   for (int c = threadIdx.x; c < d; c += blockDim.x) {
-    double s = 0.0;
-    for (int J = 0; J < nb; ++J) s += vis_part[((size_t)g * nb + J) * d + c];
+    double part[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    int J = 0;
+    for (; J + 8 <= nb; J += 8) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) part[u] += vis_part[((size_t)g * nb + J + u) * d + c];
+    }
+    for (; J < nb; ++J) part[0] += vis_part[((size_t)g * nb + J) * d + c];
+    const double s = ((part[0] + part[1]) + (part[2] + part[3])) + ((part[4] + part[5]) + (part[6] + part[7]));
     k_act[(size_t)g * d + c] = s / static_cast<double>(n_vision);
     k_lazy[(size_t)g * d + c] = to_f64(K[((size_t)g * N + sink) * d + c]);
   }
@@ -90,12 +122,15 @@ __global__ void probe_finish_kernel(const T* __restrict__ K, int N, int d, int n
 
 // ------------------------------------------------------------------------ K2
 // CTA (block J, q head h), 8 warps. A row is read by LPR = d/8 lanes with one
-// 16-byte (bf16) vector load each, so a warp covers 32/LPR rows per step with
-// fully coalesced 256-byte row segments. Two f64 dot products per row (lazy /
-// active probe keys) are reduced over the LPR lanes; the group leader applies
-// the reference's max-subtracted two-way softmax and the strict p_act > tau
-// test (query_select.py:63-68). Column sums for the pooled query stay in
-// registers and are reduced across lanes and warps once at the end.
+// 16-byte (bf16) vector load each (a coalesced 256-byte row segment); every
+// lane keeps U = 4 rows in flight so the pass streams at HBM rate. Two f64 dot
+// products per row (lazy / active probe keys) are butterfly-reduced over the
+// LPR lanes, after which lane k of the row group finalises row k: the
+// reference's max-subtracted two-way softmax (one of the two exponentials is
+// exp(0) = 1) and the strict p_act > tau test (query_select.py:63-68). Column
+// sums for the pooled query stay in registers until the end.
+constexpr int QS_U = 4;
+
 template <typename T>
 __global__ void __launch_bounds__(256) q_score_kernel(const T* __restrict__ Q, int N, int d, int rep, int n_vision,
                                                       double tau, int preserve, int block,
@@ -112,7 +147,7 @@ __global__ void __launch_bounds__(256) q_score_kernel(const T* __restrict__ Q, i
   const int lpr = d / 8;                 // lanes per row
   const int rpw = 32 / lpr;              // rows per warp step
   const int sub = lane / lpr, cl = lane % lpr;
-  const int slots = 8 * rpw;             // rows in flight per CTA step
+  const int slots = 8 * rpw;             // row slots per CTA
   const int slot = warp * rpw + sub;
   const int r0 = J * block, r1 = min(N, r0 + block);
   const double scale = 1.0 / sqrt(static_cast<double>(d));
@@ -125,44 +160,63 @@ __global__ void __launch_bounds__(256) q_score_kernel(const T* __restrict__ Q, i
   }
   int cnt = 0;
   const T* qh = Q + (size_t)h * N * d + cl * 8;
-  for (int rb = r0; rb < r1; rb += slots) {
-    const int r = rb + slot;
-    const bool valid = r < r1;
-    double x[8];
-    if (valid) {
-      Vec8<T>::load(qh + (size_t)r * d, x);
-    } else {
+  for (int rb = r0; rb < r1; rb += slots * QS_U) {
+    Raw8<T> x[QS_U];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) x[i] = 0.0;
+    for (int u = 0; u < QS_U; ++u) {
+      const int r = rb + u * slots + slot;
+      if (r < r1) x[u].load(qh + (size_t)r * d); else x[u].zero();
     }
-    double dl = 0.0, da = 0.0;
+    double dl[QS_U], da[QS_U];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      pool[i] += x[i];
-      dl = fma(x[i], kl[i], dl);
-      da = fma(x[i], ka[i], da);
+    for (int u = 0; u < QS_U; ++u) {
+      dl[u] = 0.0;
+      da[u] = 0.0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const double v = x[u].at(i);
+        pool[i] += v;
+        dl[u] = fma(v, kl[i], dl[u]);
+        da[u] = fma(v, ka[i], da[u]);
+      }
     }
     for (int o = lpr >> 1; o > 0; o >>= 1) {
-      dl += __shfl_xor_sync(0xffffffffu, dl, o);
-      da += __shfl_xor_sync(0xffffffffu, da, o);
+#pragma unroll
+      for (int u = 0; u < QS_U; ++u) {
+        dl[u] += __shfl_xor_sync(0xffffffffu, dl[u], o);
+        da[u] += __shfl_xor_sync(0xffffffffu, da[u], o);
+      }
     }
-    if (!valid) continue;
-    int act = 1;
-    if (r < n_vision) {
-      const double l0 = dl * scale, l1 = da * scale;
-      const double mx = fmax(l0, l1);
-      const double e0 = exp(l0 - mx), e1 = exp(l1 - mx);
-      const double p = e1 / (e0 + e1);
-      act = (p > tau) ? 1 : 0;
-      if (cl == 0 && p_act) p_act[(size_t)h * n_vision + r] = p;
+    // lane cl == u of the row group finalises row u of this step
+    int my_act = 1;
+    const int ur = cl < QS_U ? cl : 0;
+    const int r_mine = rb + ur * slots + slot;
+    if (cl < QS_U && r_mine < r1) {
+      double l0 = dl[0], l1 = da[0];
+#pragma unroll
+      for (int u = 1; u < QS_U; ++u)
+        if (u == cl) { l0 = dl[u]; l1 = da[u]; }
+      if (r_mine < n_vision) {
+        l0 *= scale;
+        l1 *= scale;
+        const double p = (l1 >= l0) ? 1.0 / (exp(l0 - l1) + 1.0) : (exp(l1 - l0) / (1.0 + exp(l1 - l0)));
+        my_act = (p > tau) ? 1 : 0;
+        if (p_act) p_act[(size_t)h * n_vision + r_mine] = p;
+      }
+      if (preserve && h == 0) my_act = 1;
+      active[(size_t)h * N + r_mine] = static_cast<uint8_t>(my_act);
+      cnt += my_act;
     }
-    if (preserve && h == 0) act = 1;
-    if (cl == 0) {
-      active[(size_t)h * N + r] = static_cast<uint8_t>(act);
-      cnt += act;
+    if (o_zero) {
+#pragma unroll
+      for (int u = 0; u < QS_U; ++u) {
+        const int src_lane = sub * lpr + u;
+        const int act_u = __shfl_sync(0xffffffffu, my_act, src_lane);
+        const int r = rb + u * slots + slot;
+        if (r < r1 && !act_u)
+          *reinterpret_cast<uint4*>(o_zero + ((size_t)h * N + r) * d + cl * 8) = make_uint4(0, 0, 0, 0);
+      }
     }
-    if (!act && o_zero)
-      *reinterpret_cast<uint4*>(o_zero + ((size_t)h * N + r) * d + cl * 8) = make_uint4(0, 0, 0, 0);
   }
 #pragma unroll
   for (int i = 0; i < 8; ++i) s_pool[slot * d + cl * 8 + i] = pool[i];

@@ -49,9 +49,16 @@ __global__ void __launch_bounds__(256) probe_scores_kernel(const double* __restr
     for (int u = 0; u < 2; ++u) {
       const int jj = tj + 16 * u, J = jt + jj;
       if (I < nb && J <= I) {
-        double acc = 0.0;
-        for (int c = 0; c < d; ++c) acc = fma(sq[ti * ld + c], sk[jj * ld + c], acc);
-        S[((size_t)h * nb + I) * nb + J] = acc * scale;
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        int c = 0;
+        for (; c + 4 <= d; c += 4) {
+          a0 = fma(sq[ti * ld + c], sk[jj * ld + c], a0);
+          a1 = fma(sq[ti * ld + c + 1], sk[jj * ld + c + 1], a1);
+          a2 = fma(sq[ti * ld + c + 2], sk[jj * ld + c + 2], a2);
+          a3 = fma(sq[ti * ld + c + 3], sk[jj * ld + c + 3], a3);
+        }
+        for (; c < d; ++c) a0 = fma(sq[ti * ld + c], sk[jj * ld + c], a0);
+        S[((size_t)h * nb + I) * nb + J] = ((a0 + a1) + (a2 + a3)) * scale;
       }
     }
   }
@@ -74,26 +81,42 @@ __global__ void probe_rowstats_kernel(const double* __restrict__ S, int nb, doub
   }
 }
 
-// mass[h, J] = sum over rows I >= J (ascending, like the reference colsum) of
-// exp(S[I, J] - max_I) / sum_I.
-__global__ void probe_colsum_kernel(const double* __restrict__ S, const double* __restrict__ stats, int nb,
-                                    double* __restrict__ mass) {
+// mass[h, J] = sum over rows I >= J of exp(S[I, J] - max_I) / sum_I. Block of
+// 32 columns x 8 row-phases: each thread sums the rows I = J + phase mod 8 (8
+// independent loads in flight), partials are combined in a fixed order.
+__global__ void __launch_bounds__(256) probe_colsum_kernel(const double* __restrict__ S,
+                                                           const double* __restrict__ stats, int nb,
+                                                           double* __restrict__ mass) {
+  __shared__ double part[8][33];
   const int h = blockIdx.y;
-  const int J = blockIdx.x * blockDim.x + threadIdx.x;
-  if (J >= nb) return;
+  const int cj = threadIdx.x & 31, ph = threadIdx.x >> 5;
+  const int J = blockIdx.x * 32 + cj;
   double acc = 0.0;
-  for (int I = J; I < nb; ++I) {
-    const double* st = stats + ((size_t)h * nb + I) * 2;
-    acc += exp(S[((size_t)h * nb + I) * nb + J] - st[0]) / st[1];
+  if (J < nb) {
+    const double* Sh = S + (size_t)h * nb * nb;
+    const double* st = stats + (size_t)h * nb * 2;
+    for (int I = J + ph; I < nb; I += 8) acc += exp(Sh[(size_t)I * nb + J] - st[2 * I]) / st[2 * I + 1];
   }
-  mass[(size_t)h * nb + J] = acc;
+  part[ph][cj] = acc;
+  __syncthreads();
+  if (ph == 0 && J < nb) {
+    double t = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) t += part[k][cj];
+    mass[(size_t)h * nb + J] = t;
+  }
 }
 
 // ----------------------------------------------------------------------- K3b
 struct SelShared {
   double key[kSelMaxBlocks];
+  double pre[kSelMaxBlocks];
   int idx[kSelMaxBlocks];
   int take[kSelMaxBlocks];
+  int ipre[kSelMaxBlocks];
+  double wtot[32];
+  int itot[32];
+  int cross;
   double red[32];
   double kurt[64];
   int flat;
@@ -119,6 +142,41 @@ __device__ double block_reduce_sum(double v, double* red) {
   t = red[0];
   __syncthreads();
   return t;
+}
+
+// In-place inclusive prefix sum of a[0..n) (smem) with the whole block:
+// contiguous per-thread runs, warp shuffles, then warp totals.
+template <typename T>
+__device__ void block_inclusive_scan(T* a, int n, T* tot) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int per = (n + blockDim.x - 1) / blockDim.x;
+  const int beg = min(n, threadIdx.x * per), end = min(n, beg + per);
+  T run = 0;
+  for (int i = beg; i < end; ++i) {
+    run += a[i];
+    a[i] = run;
+  }
+  T v = run;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const T y = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += y;
+  }
+  if (lane == 31) tot[warp] = v;
+  __syncthreads();
+  if (warp == 0) {
+    T w = (lane < nw) ? tot[lane] : T(0);
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const T y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    tot[lane] = w;
+  }
+  __syncthreads();
+  const T off = (v - run) + (warp > 0 ? tot[warp - 1] : T(0));
+  for (int i = beg; i < end; ++i) a[i] += off;
+  __syncthreads();
 }
 
 // Ascending bitonic sort of (key, idx) pairs, ties broken by idx: with
@@ -200,34 +258,34 @@ __global__ void __launch_bounds__(1024) select_kernel(const double* __restrict__
     }
     __syncthreads();
     bitonic_sort(S.key, S.idx, np2);
+    for (int i = threadIdx.x; i < nb; i += blockDim.x)
+      S.pre[i] = static_cast<double>(block_len(S.idx[i], N, B)) * (-S.key[i]);
+    if (threadIdx.x == 0) S.cross = nb - 1;
+    __syncthreads();
+    block_inclusive_scan(S.pre, nb, S.wtot);  // descending-sorted cumulative mass, block-wise
+    const double total = S.pre[nb - 1];
+    const double thr = fmin(p * total, total);
+    for (int i = threadIdx.x; i < nb; i += blockDim.x)
+      if (S.pre[i] >= thr) atomicMin(&S.cross, i);
+    __syncthreads();
     if (threadIdx.x == 0) {
-      double total = 0.0;
-      for (int i = 0; i < nb; ++i) total += static_cast<double>(block_len(S.idx[i], N, B)) * (-S.key[i]);
-      const double thr = fmin(p * total, total);
-      double C = 0.0;
-      int T = 0, b = N;
-      double ret = total;
-      for (int i = 0; i < nb; ++i) {
-        const double s = -S.key[i];
-        const int len = block_len(S.idx[i], N, B);
-        const double end = C + static_cast<double>(len) * s;
-        if (end >= thr || i == nb - 1) {
-          int k = 1;
-          if (s > 0.0) {
-            double kk = ceil((thr - C) / s);
-            k = (kk < 1.0) ? 1 : (kk > len ? len : static_cast<int>(kk));
-            while (k > 1 && C + static_cast<double>(k - 1) * s >= thr) --k;
-            while (k < len && C + static_cast<double>(k) * s < thr) ++k;
-          }
-          b = T + k;
-          ret = C + static_cast<double>(k) * s;
-          break;
-        }
-        C = end;
-        T += len;
+      const int i = S.cross;
+      const double s = -S.key[i];
+      const int len = block_len(S.idx[i], N, B);
+      const double C = i > 0 ? S.pre[i - 1] : 0.0;
+      int T = 0;
+      for (int t = 0; t < i; ++t) T += block_len(S.idx[t], N, B);
+      int k = len;
+      if (s > 0.0) {
+        const double kk = ceil((thr - C) / s);
+        k = (kk < 1.0) ? 1 : (kk > len ? len : static_cast<int>(kk));
+        while (k > 1 && C + static_cast<double>(k - 1) * s >= thr) --k;
+        while (k < len && C + static_cast<double>(k) * s < thr) ++k;
+      } else {
+        k = 1;
       }
-      S.budget = b;
-      S.retained = ret;
+      S.budget = T + k;
+      S.retained = C + static_cast<double>(k) * s;
       S.total = total;
     }
   }
@@ -252,22 +310,22 @@ __global__ void __launch_bounds__(1024) select_kernel(const double* __restrict__
     }
     __syncthreads();
     bitonic_sort(S.key, S.idx, np2);
-    if (threadIdx.x == 0) {
-      int left = b;
-      for (int i = 0; i < nb && left > 0; ++i) {
-        const int J = S.idx[i];
-        const int lo = J * B;
-        const int len = max(0, min(lo + block_len(J, N, B), span) - lo);
-        const int t = min(len, left);
-        S.take[J] = t;
-        left -= t;
-      }
-      int off = 0;  // exclusive prefix over blocks in index order (reuse idx[])
-      for (int J = 0; J < nb; ++J) {
-        S.idx[J] = off;
-        off += S.take[J];
-      }
+    for (int i = threadIdx.x; i < nb; i += blockDim.x) {
+      const int lo = S.idx[i] * B;
+      S.ipre[i] = max(0, min(lo + block_len(S.idx[i], N, B), span) - lo);  // vision-clipped length
     }
+    __syncthreads();
+    block_inclusive_scan(S.ipre, nb, S.itot);
+    for (int i = threadIdx.x; i < nb; i += blockDim.x) {
+      const int len = S.ipre[i] - (i > 0 ? S.ipre[i - 1] : 0);
+      const int before = S.ipre[i] - len;
+      S.take[S.idx[i]] = max(0, min(len, b - before));  // whole blocks in rank order, marginal prefix
+    }
+    __syncthreads();
+    for (int J = threadIdx.x; J < nb; J += blockDim.x) S.ipre[J] = S.take[J];
+    __syncthreads();
+    block_inclusive_scan(S.ipre, nb, S.itot);
+    for (int J = threadIdx.x; J < nb; J += blockDim.x) S.idx[J] = S.ipre[J] - S.take[J];  // exclusive offsets
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
     for (int J = warp; J < nb; J += nw) {
@@ -312,7 +370,7 @@ extern "C" int omni_probe_mass(const double* pooled_q, const double* pooled_k, i
   probe_scores_kernel<<<dim3((n_blocks + 15) / 16, n_q_heads), 256, shm, s>>>(pooled_q, pooled_k, n_blocks, head_dim,
                                                                             n_q_heads / n_kv_heads, S);
   probe_rowstats_kernel<<<dim3(n_blocks, n_q_heads), 32, 0, s>>>(S, n_blocks, st);
-  probe_colsum_kernel<<<dim3((n_blocks + 127) / 128, n_q_heads), 128, 0, s>>>(S, st, n_blocks, mass);
+  probe_colsum_kernel<<<dim3((n_blocks + 31) / 32, n_q_heads), 256, 0, s>>>(S, st, n_blocks, mass);
   return omni_launch_check();
 }
 
