@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-train", action="store_true")
     ap.add_argument("--no-knobs", action="store_true", help="skip the second-operating-point sweep")
     ap.add_argument("--flashinfer", action="store_true", help="also time flashinfer's dense FMHA (JIT)")
     return ap.parse_args()
@@ -336,6 +337,56 @@ def decode_section(args, steps, warmup, hbm_peak):
     return res
 
 
+# ------------------------------------------------------------------ training (C4)
+def train_section(args, steps, warmup, tc_peak):
+    """Config C4: sparse attention forward + backward at 32K tokens (28/4
+    heads), selection under no_grad, vs cuDNN SDPA forward + backward."""
+    import torch
+
+    from paper_2511_12201_b200.autograd import SparseAttentionFn, plan_from_selection
+    from paper_2511_12201_b200.pipeline import SparsityConfig, select_device
+    from paper_2511_12201_b200.synthetic import generate_device
+
+    n = 32768
+    nv = n - N_TEXT
+    cfg = SparsityConfig(tau=args.tau, p=args.p)
+    Q, K, V = generate_device(HQ, HKV, D, nv, N_TEXT, seed=3, lazy_fraction=args.lazy)
+    Q.requires_grad_(True)
+    K.requires_grad_(True)
+    V.requires_grad_(True)
+    dO = torch.randn_like(Q)
+
+    def sparse_step():
+        with torch.no_grad():
+            _, _, _, _, _, _, rows, counts, _, sel = select_device(Q.detach(), K.detach(), nv, cfg)
+        O = SparseAttentionFn.apply(Q, K, V, plan_from_selection(rows, counts, sel, 0))
+        O.backward(dO)
+        return rows, counts, sel
+
+    rows, counts, sel = sparse_step()
+    ms = time_cuda(sparse_step, steps, warmup)
+    res = {"workload": f"sparse attention fwd+bwd, {HQ}/{HKV} heads, d={D}, {n} tokens (C4)", "ms_per_step": ms,
+           "tok_s": n / (ms / 1e3)}
+    try:
+        from torch.nn.attention import SDPBackend, sdpa_kernel
+
+        q4, k4, v4 = (x.detach().unsqueeze(0).requires_grad_(True) for x in (Q, K, V))
+        g4 = dO.unsqueeze(0)
+
+        def dense_step():
+            with sdpa_kernel(SDPBackend.CUDNN_ATTENTION):
+                o = torch.nn.functional.scaled_dot_product_attention(q4, k4, v4, is_causal=True, enable_gqa=True)
+            o.backward(g4)
+
+        dense_step()
+        dms = time_cuda(dense_step, steps, warmup)
+        res["dense_cudnn_fwd_bwd_ms"] = dms
+        res["speedup_vs_dense"] = dms / ms
+    except Exception as e:  # noqa: BLE001
+        res["dense_error"] = str(e)[:160]
+    return res
+
+
 # ------------------------------------------------------------------ main arms
 def run_ours(args):
     import torch
@@ -488,6 +539,14 @@ def run_ours(args):
             except Exception as e:  # noqa: BLE001
                 line["cpu_baseline"] = {"error": str(e)[:200]}
         log("decode section")
+        # ----- training step (C4: fwd + bwd at 32K)
+        if not args.no_train:
+            log("train section")
+            try:
+                line["train"] = train_section(args, max(3, args.steps // 2), 2, tc_peak)
+            except Exception as e:  # noqa: BLE001
+                line["train"] = {"error": str(e)[:300]}
+            torch.cuda.empty_cache()
         # ----- decode (C5 shape at 1 GPU, sequence-sharded across ranks at N>1)
         if not args.no_decode:
             del res
