@@ -274,32 +274,38 @@ sparse_fwd_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constan
             }
           }
         }
-        float rs0 = 0.f, rs1 = 0.f;
+        // Pass 2: packed-fp32 (FFMA2 / FADD2) exponent arguments and row sums;
+        // one pair in four takes the polynomial exp2 on the FMA pipe.
+        const uint64_t c2 = f32x2(sl2, sl2), n2 = f32x2(nmu, nmu);
+        uint64_t acc0 = f32x2(0.f, 0.f), acc1 = f32x2(0.f, 0.f);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {  // pass 2: 32 keys per chunk -> 16 bf16 pairs over S columns [16q, 16q+16)
+        for (int q = 0; q < 4; ++q) {  // 32 keys per chunk -> 16 bf16 pairs over S columns [16q, 16q+16)
           uint32_t sr[32], pk[16];
           __syncwarp();
           tmem_ld32(tl + col_s(x) + q * 32, sr);  // columns >= 32q: not yet overwritten by P
           tmem_wait_ld();
-          if (!full) {
+          if (!full) {  // staircase tile: masked keys -> -inf -> exactly 0 below
 #pragma unroll
             for (int c = 0; c < 32; ++c)
               if (q * 32 + c >= lim) sr[c] = __float_as_uint(-INFINITY);
           }
 #pragma unroll
           for (int c = 0; c < 32; c += 2) {
-            const float x0 = fmaf(__uint_as_float(sr[c]), sl2, nmu);
-            const float x1 = fmaf(__uint_as_float(sr[c + 1]), sl2, nmu);
-            const float p0 = ((c & 15) >= 12) ? exp2_poly(x0) : fast_exp2(x0);
-            const float p1 = ((c & 15) >= 12) ? exp2_poly(x1) : fast_exp2(x1);
-            rs0 += p0;
-            rs1 += p1;
-            pk[c >> 1] = pack_bf16x2(p0, p1);
+            const uint64_t xx = ffma2(f32x2(__uint_as_float(sr[c]), __uint_as_float(sr[c + 1])), c2, n2);
+            uint64_t pp;
+            if ((c & 7) == 6) {
+              pp = exp2_poly2(xx);
+            } else {
+              pp = f32x2(fast_exp2(f32x2_lo(xx)), fast_exp2(f32x2_hi(xx)));
+            }
+            if ((c & 2) == 0) acc0 = fadd2(acc0, pp); else acc1 = fadd2(acc1, pp);
+            pk[c >> 1] = pack_bf16x2(f32x2_lo(pp), f32x2_hi(pp));
           }
           __syncwarp();
           tmem_st16(tl + col_s(x) + q * 16, pk);
         }
-        l_run = l_run * alpha + (rs0 + rs1);
+        const uint64_t acc = fadd2(acc0, acc1);
+        l_run = l_run * alpha + (f32x2_lo(acc) + f32x2_hi(acc));
         tmem_wait_st();
         tc_fence_before();
         mbar_arrive(B(B_PF + x));

@@ -255,6 +255,51 @@ __device__ __forceinline__ float exp2_poly(float x) {
   return zero ? 0.f : v;
 }
 
+// ---- packed fp32 pairs (sm_100 FFMA2 / FADD2): lo = first element
+__device__ __forceinline__ uint64_t f32x2(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ float f32x2_lo(uint64_t v) {
+  float lo, hi;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+  return lo;
+}
+__device__ __forceinline__ float f32x2_hi(uint64_t v) {
+  float lo, hi;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+  return hi;
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+// exp2 of a pair on the FMA pipe (same polynomial as exp2_poly); arguments
+// below -126 (masked -inf included) give exactly 0.
+__device__ __forceinline__ uint64_t exp2_poly2(uint64_t x) {
+  const float xl = f32x2_lo(x), xh = f32x2_hi(x);
+  float lo = fmaxf(xl, -126.f), hi = fmaxf(xh, -126.f);
+  const uint64_t xc = f32x2(lo, hi);
+  const uint64_t magic = f32x2(12582912.f, 12582912.f), nmagic = f32x2(-12582912.f, -12582912.f);
+  const uint64_t r = fadd2(xc, magic);            // integer part in the low mantissa bits
+  const uint64_t f = fadd2(xc, fadd2(r, nmagic) ^ 0x8000000080000000ull);  // x - (r - magic), in [-0.5, 0.5]
+  uint64_t p = ffma2(f32x2(0.05517165f, 0.05517165f), f, f32x2(0.24261116f, 0.24261116f));
+  p = ffma2(p, f, f32x2(0.69326099f, 0.69326099f));
+  p = ffma2(p, f, f32x2(0.99992807f, 0.99992807f));
+  // scale by 2^n: (bits(r) - bits(magic)) << 23 == bits(r) << 23 (mod 2^32)
+  const uint32_t rl = static_cast<uint32_t>(r), rh = static_cast<uint32_t>(r >> 32);
+  const uint32_t pl = static_cast<uint32_t>(p), ph = static_cast<uint32_t>(p >> 32);
+  const uint32_t ol = xl < -126.f ? 0u : pl + (rl << 23), oh = xh < -126.f ? 0u : ph + (rh << 23);
+  return (static_cast<uint64_t>(oh) << 32) | static_cast<uint64_t>(ol);
+}
+
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }

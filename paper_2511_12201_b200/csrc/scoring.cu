@@ -105,17 +105,21 @@ template <typename T>
 __global__ void probe_finish_kernel(const T* __restrict__ K, int N, int d, int nb, int n_vision, int sink,
                                     const double* __restrict__ vis_part, double* __restrict__ k_lazy,
                                     double* __restrict__ k_act) {
-  const int g = blockIdx.x;
-  for (int c = threadIdx.x; c < d; c += blockDim.x) {
-    double part[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    int J = 0;
-    for (; J + 8 <= nb; J += 8) {
-#pragma unroll
-      for (int u = 0; u < 8; ++u) part[u] += vis_part[((size_t)g * nb + J + u) * d + c];
-    }
-    for (; J < nb; ++J) part[0] += vis_part[((size_t)g * nb + J) * d + c];
-    const double s = ((part[0] + part[1]) + (part[2] + part[3])) + ((part[4] + part[5]) + (part[6] + part[7]));
-    k_act[(size_t)g * d + c] = s / static_cast<double>(n_vision);
+  // CTA (32-column slice, group g), 1024 threads = 32 columns x 32 block phases;
+  // partial sums over blocks J = phase (mod 32), combined in a fixed order.
+  __shared__ double part[32][33];
+  const int g = blockIdx.y;
+  const int col = threadIdx.x & 31, ph = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + col;
+  double s = 0.0;
+  if (c < d)
+    for (int J = ph; J < nb; J += 32) s += vis_part[((size_t)g * nb + J) * d + c];
+  part[ph][col] = s;
+  __syncthreads();
+  if (ph == 0 && c < d) {
+    double t = 0.0;
+    for (int k = 0; k < 32; ++k) t += part[k][col];
+    k_act[(size_t)g * d + c] = t / static_cast<double>(n_vision);
     k_lazy[(size_t)g * d + c] = to_f64(K[((size_t)g * N + sink) * d + c]);
   }
 }
@@ -329,13 +333,13 @@ extern "C" int omni_kv_probe(const void* K, int dtype, int n_kv_heads, int seq_l
   if (dtype == OMNI_DTYPE_BF16) {
     kv_probe_kernel<__nv_bfloat16><<<grid, 256, shm, s>>>(static_cast<const __nv_bfloat16*>(K), seq_len, head_dim,
                                                             n_vision, block_size, pooled_k, vis);
-    probe_finish_kernel<__nv_bfloat16><<<n_kv_heads, 128, 0, s>>>(static_cast<const __nv_bfloat16*>(K), seq_len,
+    probe_finish_kernel<__nv_bfloat16><<<dim3((head_dim + 31) / 32, n_kv_heads), 1024, 0, s>>>(static_cast<const __nv_bfloat16*>(K), seq_len,
                                                                    head_dim, nb, n_vision, sink_index, vis, k_lazy,
                                                                    k_act);
   } else if (dtype == OMNI_DTYPE_F32) {
     kv_probe_kernel<float><<<grid, 256, shm, s>>>(static_cast<const float*>(K), seq_len, head_dim, n_vision,
                                                     block_size, pooled_k, vis);
-    probe_finish_kernel<float><<<n_kv_heads, 128, 0, s>>>(static_cast<const float*>(K), seq_len, head_dim, nb,
+    probe_finish_kernel<float><<<dim3((head_dim + 31) / 32, n_kv_heads), 1024, 0, s>>>(static_cast<const float*>(K), seq_len, head_dim, nb,
                                                            n_vision, sink_index, vis, k_lazy, k_act);
   } else {
     OMNI_CHECK(false, OMNI_E_PARAM, "unsupported dtype");
