@@ -224,39 +224,71 @@ sparse_fwd_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constan
       for (int j = 0; j < nt; ++j) {
         mbar_wait(B(B_SF + x), j & 1);
         tc_fence_after();
-        // Pass 1: row max over the four 32-column chunks of S (registers stay
-        // small: S is re-read from TMEM in pass 2 instead of held as 128 regs).
         const int lim = vis - j * BN;
         const bool full = __all_sync(0xffffffffu, lim >= BN);
-        float m0 = -INFINITY, m1 = -INFINITY, m2 = -INFINITY, m3 = -INFINITY;
+        // One pass over S in four 32-column TMEM chunks: raw row max and, when
+        // `do_exp`, the exponentials against the current (possibly stale)
+        // max, packed bf16 into pk[] and summed into the return value.
+        uint32_t pk[64];
+        auto pass = [&](float nmu, bool do_exp, float& mt) -> float {
+          const uint64_t c2 = f32x2(sl2, sl2), n2 = f32x2(nmu, nmu);
+          uint64_t acc0 = f32x2(0.f, 0.f), acc1 = f32x2(0.f, 0.f);
+          float m0 = -INFINITY, m1 = -INFINITY;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          uint32_t sr[32];
-          __syncwarp();
-          tmem_ld32(tl + col_s(x) + q * 32, sr);
-          tmem_wait_ld();
-          if (!full) {
+          for (int q = 0; q < 4; ++q) {
+            uint32_t sr[32];
+            __syncwarp();
+            tmem_ld32(tl + col_s(x) + q * 32, sr);
+            tmem_wait_ld();
+            if (!full) {  // staircase tile: masked keys -> -inf -> exactly 0
 #pragma unroll
-            for (int c = 0; c < 32; ++c)
-              if (q * 32 + c >= lim) sr[c] = __float_as_uint(-INFINITY);
+              for (int c = 0; c < 32; ++c)
+                if (q * 32 + c >= lim) sr[c] = __float_as_uint(-INFINITY);
+            }
+#pragma unroll
+            for (int c = 0; c < 32; c += 4) {
+              m0 = fmax3(m0, __uint_as_float(sr[c]), __uint_as_float(sr[c + 1]));
+              m1 = fmax3(m1, __uint_as_float(sr[c + 2]), __uint_as_float(sr[c + 3]));
+            }
+            if (do_exp) {
+#pragma unroll
+              for (int c = 0; c < 32; c += 2) {
+                const uint64_t xx = ffma2(f32x2(__uint_as_float(sr[c]), __uint_as_float(sr[c + 1])), c2, n2);
+                uint64_t pp;
+                if ((c & 7) == 6) {
+                  pp = exp2_poly2(xx);  // one pair in four on the FMA pipe (MUFU relief)
+                } else {
+                  pp = f32x2(fast_exp2(f32x2_lo(xx)), fast_exp2(f32x2_hi(xx)));
+                }
+                if ((c & 2) == 0) acc0 = fadd2(acc0, pp); else acc1 = fadd2(acc1, pp);
+                pk[q * 16 + (c >> 1)] = pack_bf16x2(f32x2_lo(pp), f32x2_hi(pp));
+              }
+            }
           }
-#pragma unroll
-          for (int c = 0; c < 32; c += 8) {
-            m0 = fmax3(m0, __uint_as_float(sr[c]), __uint_as_float(sr[c + 1]));
-            m1 = fmax3(m1, __uint_as_float(sr[c + 2]), __uint_as_float(sr[c + 3]));
-            m2 = fmax3(m2, __uint_as_float(sr[c + 4]), __uint_as_float(sr[c + 5]));
-            m3 = fmax3(m3, __uint_as_float(sr[c + 6]), __uint_as_float(sr[c + 7]));
+          mt = fmaxf(m0, m1);
+          const uint64_t acc = fadd2(acc0, acc1);
+          return f32x2_lo(acc) + f32x2_hi(acc);
+        };
+        // Speculate with the running max (no separate max pass); redo the
+        // tile only when some row's max grew by more than 2^8 (lazy rescale).
+        float rsum = 0.f, alpha = 1.f;
+        bool resc = false;
+        // a row seeing its first visible keys has no max to speculate with
+        bool do_exp = !__any_sync(0xffffffffu, m_run == -INFINITY && lim > 0);
+        for (int attempt = 0; attempt < 2; ++attempt) {
+          float mt;
+          rsum = pass(m_run == -INFINITY ? 0.f : -m_run, do_exp, mt);
+          if (attempt == 0) {
+            const float m_new = fmaxf(m_run, mt * sl2);
+            resc = m_new > m_run + 8.0f;
+            if (resc) {
+              alpha = (m_run == -INFINITY) ? 0.f : fast_exp2(m_run - m_new);
+              m_run = m_new;
+            }
           }
+          if (do_exp && !__any_sync(0xffffffffu, attempt == 0 && resc)) break;
+          do_exp = true;
         }
-        const float mt = fmaxf(fmaxf(m0, m1), fmaxf(m2, m3));
-        const float m_new = fmaxf(m_run, mt * sl2);
-        const bool resc = m_new > m_run + 8.0f;
-        float alpha = 1.f;
-        if (resc) {
-          alpha = (m_run == -INFINITY) ? 0.f : fast_exp2(m_run - m_new);
-          m_run = m_new;
-        }
-        const float nmu = (m_run == -INFINITY) ? 0.f : -m_run;
 
         if (j > 0) {
           mbar_wait(B(B_PV + x), (j - 1) & 1);  // PV_X(j-1) done: O stable
@@ -274,38 +306,11 @@ sparse_fwd_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constan
             }
           }
         }
-        // Pass 2: packed-fp32 (FFMA2 / FADD2) exponent arguments and row sums;
-        // one pair in four takes the polynomial exp2 on the FMA pipe.
-        const uint64_t c2 = f32x2(sl2, sl2), n2 = f32x2(nmu, nmu);
-        uint64_t acc0 = f32x2(0.f, 0.f), acc1 = f32x2(0.f, 0.f);
+        // P (bf16 pairs) over S columns [0, 64): the A operand of PV_X(j).
+        __syncwarp();
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {  // 32 keys per chunk -> 16 bf16 pairs over S columns [16q, 16q+16)
-          uint32_t sr[32], pk[16];
-          __syncwarp();
-          tmem_ld32(tl + col_s(x) + q * 32, sr);  // columns >= 32q: not yet overwritten by P
-          tmem_wait_ld();
-          if (!full) {  // staircase tile: masked keys -> -inf -> exactly 0 below
-#pragma unroll
-            for (int c = 0; c < 32; ++c)
-              if (q * 32 + c >= lim) sr[c] = __float_as_uint(-INFINITY);
-          }
-#pragma unroll
-          for (int c = 0; c < 32; c += 2) {
-            const uint64_t xx = ffma2(f32x2(__uint_as_float(sr[c]), __uint_as_float(sr[c + 1])), c2, n2);
-            uint64_t pp;
-            if ((c & 7) == 6) {
-              pp = exp2_poly2(xx);
-            } else {
-              pp = f32x2(fast_exp2(f32x2_lo(xx)), fast_exp2(f32x2_hi(xx)));
-            }
-            if ((c & 2) == 0) acc0 = fadd2(acc0, pp); else acc1 = fadd2(acc1, pp);
-            pk[c >> 1] = pack_bf16x2(f32x2_lo(pp), f32x2_hi(pp));
-          }
-          __syncwarp();
-          tmem_st16(tl + col_s(x) + q * 16, pk);
-        }
-        const uint64_t acc = fadd2(acc0, acc1);
-        l_run = l_run * alpha + (f32x2_lo(acc) + f32x2_hi(acc));
+        for (int q = 0; q < 4; ++q) tmem_st16(tl + col_s(x) + q * 16, pk + q * 16);
+        l_run = l_run * alpha + rsum;
         tmem_wait_st();
         tc_fence_before();
         mbar_arrive(B(B_PF + x));

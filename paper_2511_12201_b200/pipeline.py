@@ -88,6 +88,53 @@ def select_device(Q: torch.Tensor, K: torch.Tensor, n_vision: int, cfg: Sparsity
     return k_lazy, k_act, pk, active, p_act, pq, rows, counts, mass, sel
 
 
+class PrefillStreamer:
+    """Host-buffer serving API: pinned host Q/K/V in, host O out, with the
+    host<->device copies of neighbouring requests overlapped with compute.
+
+    Request i's H2D copy runs on a copy stream while request i-1 computes and
+    request i-2's output drains on a second copy stream (``depth`` device
+    buffer sets rotate). Every request still pays its own copies; only their
+    latency is hidden behind other requests' kernels."""
+
+    def __init__(self, hq: int, hkv: int, n: int, d: int, n_vision: int, cfg: SparsityConfig = SparsityConfig(),
+                 depth: int = 3, device="cuda"):
+        self.n_vision, self.cfg = n_vision, cfg
+        bf = dict(device=device, dtype=torch.bfloat16)
+        self.bufs = [dict(Q=torch.empty(hq, n, d, **bf), K=torch.empty(hkv, n, d, **bf),
+                          V=torch.empty(hkv, n, d, **bf), O=torch.empty(hq, n, d, **bf),
+                          free=torch.cuda.Event(), loaded=torch.cuda.Event(), done=torch.cuda.Event())
+                     for _ in range(depth)]
+        for b in self.bufs:
+            b["free"].record()
+        self.h2d, self.d2h = torch.cuda.Stream(), torch.cuda.Stream()
+        self.comp = torch.cuda.current_stream()
+
+    def run(self, requests, outputs) -> None:
+        """requests: iterable of pinned (Q, K, V) host tensors; outputs: pinned
+        host tensors receiving O. Returns when all copies are enqueued."""
+        for i, ((hq_, hk_, hv_), ho) in enumerate(zip(requests, outputs)):
+            b = self.bufs[i % len(self.bufs)]
+            self.h2d.wait_event(b["free"])
+            with torch.cuda.stream(self.h2d):
+                b["Q"].copy_(hq_, non_blocking=True)
+                b["K"].copy_(hk_, non_blocking=True)
+                b["V"].copy_(hv_, non_blocking=True)
+                b["loaded"].record()
+            self.comp.wait_event(b["loaded"])
+            with torch.cuda.stream(self.comp):
+                sparse_prefill_device(b["Q"], b["K"], b["V"], self.n_vision, self.cfg, out=b["O"])
+                b["done"].record()
+            self.d2h.wait_event(b["done"])
+            with torch.cuda.stream(self.d2h):
+                ho.copy_(b["O"], non_blocking=True)
+                b["free"].record()
+
+    def synchronize(self) -> None:
+        self.d2h.synchronize()
+        self.comp.synchronize()
+
+
 def sparse_prefill_device(Q: torch.Tensor, K: torch.Tensor, V: torch.Tensor, n_vision: int,
                           cfg: SparsityConfig = SparsityConfig(), want_prob: bool = False,
                           out: torch.Tensor | None = None) -> DevicePrefill:
