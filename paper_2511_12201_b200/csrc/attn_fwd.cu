@@ -31,6 +31,7 @@
 // with no visible key copy V[g, sink] (prefill.py:119-120); LSE side output
 // for the backward kernel.
 #include <math.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 
@@ -66,6 +67,17 @@ __device__ __forceinline__ uint32_t swz(uint32_t row, uint32_t chunk16) {
   return row * 128u + ((chunk16 ^ (row & 7u)) << 4);
 }
 
+// POLY: share of exponential pairs evaluated by the FMA-pipe polynomial
+// (0: none, 1: one pair in four, 2: one in eight, 3: one in two).
+template <int POLY>
+__device__ __forceinline__ bool use_poly(int c) {
+  if constexpr (POLY == 0) return false;
+  if constexpr (POLY == 1) return (c & 7) == 6;
+  if constexpr (POLY == 2) return (c & 15) == 14;
+  return (c & 7) >= 4;
+}
+
+template <int POLY>
 __global__ void __launch_bounds__(320, 1)
 sparse_fwd_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
                   const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __restrict__ Vorig,
@@ -255,7 +267,7 @@ sparse_fwd_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constan
               for (int c = 0; c < 32; c += 2) {
                 const uint64_t xx = ffma2(f32x2(__uint_as_float(sr[c]), __uint_as_float(sr[c + 1])), c2, n2);
                 uint64_t pp;
-                if ((c & 7) == 6) {
+                if (use_poly<POLY>(c)) {
                   pp = exp2_poly2(xx);  // one pair in four on the FMA pipe (MUFU relief)
                 } else {
                   pp = f32x2(fast_exp2(f32x2_lo(xx)), fast_exp2(f32x2_hi(xx)));
@@ -380,15 +392,24 @@ extern "C" int omni_sparse_attn_fwd(const void* Q, const void* K_sel, const void
   if (st) return st;
   st = omni_make_tmap_rows(&tv, V_sel, (uint64_t)n_kv_heads * cap, 128, 2, 64, fwd::BN);
   if (st) return st;
-  static bool attr_set = false;
-  if (!attr_set) {
-    OMNI_CUDA_TRY(cudaFuncSetAttribute(fwd::sparse_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)fwd::SMEM_BYTES));
-    attr_set = true;
+  // Tuning knob for the exp2 MUFU / FMA split (OMNI_FWD_POLY = 0..3, default 1).
+  static int poly = [] {
+    const char* e = getenv("OMNI_FWD_POLY");
+    const int v = e ? atoi(e) : 1;
+    return (v >= 0 && v <= 3) ? v : 1;
+  }();
+  auto kern = poly == 0 ? fwd::sparse_fwd_kernel<0>
+            : poly == 2 ? fwd::sparse_fwd_kernel<2>
+            : poly == 3 ? fwd::sparse_fwd_kernel<3>
+                        : fwd::sparse_fwd_kernel<1>;
+  static bool attr_set[4] = {false, false, false, false};
+  if (!attr_set[poly]) {
+    OMNI_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fwd::SMEM_BYTES));
+    attr_set[poly] = true;
   }
   const int n_tiles = (seq_len + 2 * fwd::BM - 1) / (2 * fwd::BM);
   dim3 grid(n_tiles * n_q_heads);
-  fwd::sparse_fwd_kernel<<<grid, 320, fwd::SMEM_BYTES, static_cast<cudaStream_t>(stream)>>>(
+  kern<<<grid, 320, fwd::SMEM_BYTES, static_cast<cudaStream_t>(stream)>>>(
       tk, tv, static_cast<const __nv_bfloat16*>(Q), static_cast<const __nv_bfloat16*>(V), rows, counts, selected,
       sel_counts, n_q_heads, n_q_heads / n_kv_heads, seq_len, cap, seq_len, sink_index, n_tiles,
       static_cast<__nv_bfloat16*>(O), lse);
