@@ -95,6 +95,18 @@ size_t omni_probe_mass_workspace(int n_q_heads, int n_blocks);
 int omni_probe_mass(const double* pooled_q, const double* pooled_k, int n_q_heads, int n_kv_heads, int n_blocks,
                     int head_dim, double* mass, void* workspace, void* stream);
 
+/* ---------------------------------------------------------------- K3x
+ * Exact key scores (score_source = "exact"): per Q head the column mass of the
+ * full causal attention map softmax(q k^T / sqrt(d)), float64, in two passes
+ * over the causal triangle without materialising it. Replaces
+ * accumulated_key_scores over the dense oracle maps (kv_select.py:56-73,
+ * prefill.py:133-134, attention.py:99-108). Q [Hq, N, d], K [Hkv, N, d]
+ * (dtype); mass f64 [Hq, N]; workspace omni_exact_mass_workspace() bytes.
+ * O(N^2 d) float64 work: a validation-scale path (the hot path is K3a).     */
+size_t omni_exact_mass_workspace(int n_q_heads, int seq_len);
+int omni_exact_mass(const void* Q, const void* K, int dtype, int n_q_heads, int n_kv_heads, int seq_len, int head_dim,
+                    double* mass, void* workspace, void* stream);
+
 /* ---------------------------------------------------------------- K3b
  * Shared-budget KV selection from per-Q-head block column mass.
  * Replaces block_scores_to_token_scores (block_probe.py:67-78, per-token =

@@ -117,6 +117,20 @@ def probe_mass(pooled_q: torch.Tensor, pooled_k: torch.Tensor, return_workspace:
     return mass
 
 
+def exact_mass(Q: torch.Tensor, K: torch.Tensor) -> torch.Tensor:
+    """Column mass of the full causal map per Q head, f64 [Hq, N]
+    (kv_select.py:56-73 without the N^2 map)."""
+    _cuda3(Q, "Q")
+    _cuda3(K, "K")
+    if Q.dtype != K.dtype:
+        raise ShapeError("Q and K must share a dtype")
+    hq, n, d = Q.shape
+    mass = torch.empty(hq, n, device=Q.device, dtype=torch.float64)
+    ws = torch.empty(_lib.size("omni_exact_mass_workspace", hq, n), device=Q.device, dtype=torch.uint8)
+    _lib.call("omni_exact_mass", _p(Q), _p(K), _dtype(Q), hq, K.shape[0], n, d, _p(mass), _p(ws), _stream())
+    return mass
+
+
 @dataclass
 class Selection:
     """Device-resident selection (kv_select.SelectionResult + scores)."""

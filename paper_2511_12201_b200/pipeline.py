@@ -72,19 +72,39 @@ def check_qkv(Q: torch.Tensor, K: torch.Tensor, V: torch.Tensor) -> None:
 
 
 def select_device(Q: torch.Tensor, K: torch.Tensor, n_vision: int, cfg: SparsityConfig, want_prob: bool = False,
-                  O_zero: torch.Tensor | None = None):
-    """Masks + probe scores + flattest/budget/top-b (no attention)."""
+                  O_zero: torch.Tensor | None = None, score_source: str = "probe"):
+    """Masks + key scores + flattest/budget/top-b (no attention).
+
+    score_source "probe" (hot path): block-probe column masses (K3a).
+    score_source "exact": column masses of the full causal maps (K3x, O(N^2 d)
+    float64; N <= 8192 for the token-level selection)."""
     hq, n, d = Q.shape
     if not 1 <= n_vision <= n:
         raise LayoutError(f"n_vision {n_vision} outside [1, {n}]")
     if not 0 <= cfg.sink_index < n:
         raise LayoutError(f"sink_index {cfg.sink_index} outside the prompt")
+    if score_source not in ("exact", "probe"):
+        raise ParameterError("score source must be one of ('exact', 'probe')")
     k_lazy, k_act, pk = ops.kv_probe(K, n_vision, cfg.sink_index, cfg.block_size)
     active, p_act, pq, bact = ops.q_score(Q, k_lazy, k_act, n_vision, cfg.tau, cfg.preserve_first_head,
                                           cfg.block_size, want_prob=want_prob, O_zero=O_zero)
     rows, counts = ops.compact_rows(active, bact, cfg.block_size)
-    mass = ops.probe_mass(pq, pk)
-    sel = ops.select(mass, K.shape[0], n, cfg.block_size, cfg.p, cfg.granularity)
+    if score_source == "probe":
+        mass = ops.probe_mass(pq, pk)
+        sel = ops.select(mass, K.shape[0], n, cfg.block_size, cfg.p, cfg.granularity)
+    else:
+        mass = ops.exact_mass(Q, K)
+        sel = ops.select(mass, K.shape[0], n, 1, cfg.p, "token")
+        if cfg.granularity == "block":  # select_top_blocks over the same budget (kv_select.py:147-176)
+            nb = ops.n_blocks(n, cfg.block_size)
+            pad = nb * cfg.block_size - n
+            blk = torch.nn.functional.pad(mass, (0, pad)).view(hq, nb, cfg.block_size).sum(dim=2)
+            bsel = ops.select(blk, K.shape[0], n, cfg.block_size, cfg.p, "block",
+                              budget_override=int(sel.info[0]))
+            bsel.info[1] = sel.info[1]
+            bsel.stats[: K.shape[0]] = sel.stats[: K.shape[0]]
+            bsel.stats[K.shape[0]:] = sel.stats[K.shape[0]:]
+            sel = bsel
     return k_lazy, k_act, pk, active, p_act, pq, rows, counts, mass, sel
 
 
@@ -137,7 +157,7 @@ class PrefillStreamer:
 
 def sparse_prefill_device(Q: torch.Tensor, K: torch.Tensor, V: torch.Tensor, n_vision: int,
                           cfg: SparsityConfig = SparsityConfig(), want_prob: bool = False,
-                          out: torch.Tensor | None = None) -> DevicePrefill:
+                          out: torch.Tensor | None = None, score_source: str = "probe") -> DevicePrefill:
     """Full sparse prefill of one attention layer on the GPU.
 
     Q [Hq, N, 128] bf16 (or fp32 for selection-only validation — attention
@@ -149,7 +169,8 @@ def sparse_prefill_device(Q: torch.Tensor, K: torch.Tensor, V: torch.Tensor, n_v
     Kb = K if K.dtype == torch.bfloat16 else K.to(torch.bfloat16)
     Vb = V if V.dtype == torch.bfloat16 else V.to(torch.bfloat16)
     O = out if out is not None else torch.empty_like(Qb)
-    k_lazy, k_act, pk, active, p_act, pq, rows, counts, mass, sel = select_device(Q, K, n_vision, cfg, want_prob, O)
+    k_lazy, k_act, pk, active, p_act, pq, rows, counts, mass, sel = select_device(Q, K, n_vision, cfg, want_prob, O,
+                                                                                  score_source)
     cap = ops.round_up(n, ops.TILE)
     K_sel = ops.gather_rows(Kb, sel.selected, sel.counts, cap, ops.TILE)
     V_sel = ops.gather_rows(Vb, sel.selected, sel.counts, cap, ops.TILE)

@@ -51,19 +51,18 @@ class PrefillOutput:
 
 
 def sparse_prefill(w: AttentionWorkload, cfg: SparsityConfig = SparsityConfig(),
-                   score_source: str = "probe") -> PrefillOutput:
+                   score_source: str = "exact") -> PrefillOutput:
     """Query masks -> probe key scores -> flattest-group budget -> per-group
     top-b -> sparse attention (reference prefill.py:142-192 under rule B).
-    Only the block-probe score source runs on the GPU hot path; the exact
-    source needs the dense N^2 maps (SURVEY §8f "next") and is rejected."""
+    The block-probe score source is the hot path; "exact" computes the
+    dense causal maps' column masses on the GPU (K3x, O(N^2 d) float64,
+    N <= 8192) without materialising them."""
     if score_source not in SCORE_SOURCES:
         raise ParameterError(f"score source must be one of {SCORE_SOURCES}")
-    if score_source == "exact":
-        raise ParameterError("score_source='exact' needs dense attention maps; use 'probe' (block_size=1 is exact)")
     Q, K, V = w.device_tensors()
     res = sparse_prefill_device(Q, K, V, w.layout.n_vision, SparsityConfig(
         tau=cfg.tau, p=cfg.p, block_size=cfg.block_size, granularity=cfg.granularity,
-        preserve_first_head=cfg.preserve_first_head, sink_index=w.layout.sink_index))
+        preserve_first_head=cfg.preserve_first_head, sink_index=w.layout.sink_index), score_source=score_source)
     info = res.selection.info.cpu().numpy()
     stats = res.selection.stats.cpu().numpy()
     b, flat, hkv = int(info[0]), int(info[1]), K.shape[0]

@@ -183,3 +183,38 @@ def test_64k_qwen2_selection_bit_exact():
         g = h // 7
         exp = oatt.sparse_head_attention(Q[h], K[g], V[g], ref.selected[g], ref.active[h], 0, rows_subset=sample)
         np.testing.assert_allclose(out[h][sample], exp[sample], atol=ATOL, rtol=RTOL)
+
+
+@pytest.mark.parametrize("tag,gran", [("exact_token", "token"), ("exact_block", "block")])
+def test_exact_score_source_matches_reference_fixture(golden, tag, gran):
+    """score_source='exact' (K3x two-pass column mass, f64) reproduces the
+    reference's exact-path selections bit for bit (tests/golden/tiny_paths)."""
+    from paper_2511_12201_b200.pipeline import SparsityConfig, select_device
+
+    g = golden("tiny_paths.npz")
+    Q, K, V = generate(Spec(heads=4, head_dim=32, n_vision=120, n_text=8, seed=11))
+    cfg = SparsityConfig(block_size=16, granularity=gran)
+    out = select_device(to_dev(Q, torch.float32), to_dev(K, torch.float32), 120, cfg, score_source="exact")
+    active, mass, sel = out[3], out[8], out[9]
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(active.cpu().numpy().astype(bool), g[f"{tag}_active"])
+    np.testing.assert_allclose(mass.cpu().numpy(), g[f"{tag}_scores"], rtol=1e-10, atol=1e-13)
+    b = int(sel.info[0])
+    assert b == int(g[f"{tag}_budget"]) and int(sel.info[1]) == int(g[f"{tag}_flattest"])
+    np.testing.assert_array_equal(sel.selected[:, :b].cpu().numpy(), g[f"{tag}_selected"])
+
+
+def test_exact_score_source_c1_end_to_end():
+    """C1 shape through sparse_prefill(score_source='exact') vs the oracle."""
+    from paper_2511_12201_b200.pipeline import SparsityConfig, sparse_prefill_device
+
+    Q, K, V = generate(Spec(heads=4, head_dim=128, n_vision=1984, n_text=64, seed=1))
+    Q, K, V = round_bf16(Q), round_bf16(K), round_bf16(V)
+    res = sparse_prefill_device(to_dev(Q), to_dev(K), to_dev(V), 1984, SparsityConfig(), score_source="exact")
+    torch.cuda.synchronize()
+    ref = opipe.select(Q, K, 1984, 0, 0.08, 0.82, 256, score_source="exact")
+    assert int(res.selection.info[0]) == ref.budget and int(res.selection.info[1]) == ref.flattest
+    sel = res.selection.selected.cpu().numpy()
+    for g in range(4):
+        np.testing.assert_array_equal(sel[g, : ref.budget], ref.selected[g])
+    check_outputs(res, Q, K, V, ref, heads=[0, 3])
