@@ -320,7 +320,10 @@ dkv_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUt
            float* __restrict__ dV) {
   using namespace dkv;
   extern __shared__ uint8_t smem_raw[];
-  const int t = blockIdx.x, g = blockIdx.y;
+  // CTA = (key tile t, group g, Q head g*rep + rs): one Q head per CTA keeps
+  // the per-CTA work balanced (early key tiles are seen by every later row);
+  // the group's heads accumulate into dK/dV with vector fp32 reductions.
+  const int t = blockIdx.x, g = blockIdx.y / rep, rs = blockIdx.y % rep;
   const int nsel = __ldg(sel_counts + g);
   const int k0 = t * 128;
   if (k0 >= nsel) return;
@@ -338,6 +341,11 @@ dkv_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUt
     it.rep = rep;
     int tot = 0;
     for (int r = 0; r < rep; ++r) {
+      if (r != rs) {
+        it.first_tile[r] = 0;
+        it.n_tiles[r] = 0;
+        continue;
+      }
       const int h = g * rep + r;
       const int cnt = __ldg(counts + h);
       // first compact row whose position >= first_key (it sees key k0)
@@ -528,20 +536,15 @@ dkv_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUt
         tmem_ld32(tl + COL_DV + c4 * 32, a);
         tmem_ld32(tl + COL_DK + c4 * 32, b);
         tmem_wait_ld();
-        if (valid) {
+        if (valid) {  // heads of the group reduce into the zero-initialised dK / dV
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
-            dvr[c4 * 8 + q] = make_float4(__uint_as_float(a[4 * q]), __uint_as_float(a[4 * q + 1]),
-                                          __uint_as_float(a[4 * q + 2]), __uint_as_float(a[4 * q + 3]));
-            dkr[c4 * 8 + q] = make_float4(__uint_as_float(b[4 * q]) * scale, __uint_as_float(b[4 * q + 1]) * scale,
-                                          __uint_as_float(b[4 * q + 2]) * scale, __uint_as_float(b[4 * q + 3]) * scale);
+            red_add_v4(dvr + c4 * 8 + q, __uint_as_float(a[4 * q]), __uint_as_float(a[4 * q + 1]),
+                       __uint_as_float(a[4 * q + 2]), __uint_as_float(a[4 * q + 3]));
+            red_add_v4(dkr + c4 * 8 + q, __uint_as_float(b[4 * q]) * scale, __uint_as_float(b[4 * q + 1]) * scale,
+                       __uint_as_float(b[4 * q + 2]) * scale, __uint_as_float(b[4 * q + 3]) * scale);
           }
         }
-      }
-    } else if (valid) {
-      for (int q = 0; q < 32; ++q) {
-        dvr[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-        dkr[q] = make_float4(0.f, 0.f, 0.f, 0.f);
       }
     }
   }
@@ -616,7 +619,7 @@ extern "C" int omni_sparse_attn_bwd(const void* Q, const void* K_sel, const void
                                                                     visc, n_q_heads, rep, seq_len, cap, capq, n_tiles,
                                                                     dQ);
   if ((rc = omni_launch_check())) return rc;
-  bwd::dkv_kernel<<<dim3(cap / 128, n_kv_heads), 256, bwd::dkv::SMEM, st>>>(tq64, tdo64, tk, tv, rows, counts,
+  bwd::dkv_kernel<<<dim3(cap / 128, n_kv_heads * rep), 256, bwd::dkv::SMEM, st>>>(tq64, tdo64, tk, tv, rows, counts,
                                                                             selected, sel_counts, lse2c, Dc, visc, rep,
                                                                             seq_len, cap, capq, dK_sel, dV_sel);
   return omni_launch_check();

@@ -392,11 +392,13 @@ extern "C" int omni_sparse_attn_fwd(const void* Q, const void* K_sel, const void
   if (st) return st;
   st = omni_make_tmap_rows(&tv, V_sel, (uint64_t)n_kv_heads * cap, 128, 2, 64, fwd::BN);
   if (st) return st;
-  // Tuning knob for the exp2 MUFU / FMA split (OMNI_FWD_POLY = 0..3, default 1).
+  // Tuning knob for the exp2 MUFU / FMA split (OMNI_FWD_POLY = 0..3). Default
+  // 0 (all MUFU): measured fastest on B200 at 64K (11.03 ms vs 11.19 / 11.58 /
+  // 12.71 ms for 1/8, 1/4, 1/2 polynomial; profiles/r01_fa_fwd_variants.json).
   static int poly = [] {
     const char* e = getenv("OMNI_FWD_POLY");
-    const int v = e ? atoi(e) : 1;
-    return (v >= 0 && v <= 3) ? v : 1;
+    const int v = e ? atoi(e) : 0;
+    return (v >= 0 && v <= 3) ? v : 0;
   }();
   auto kern = poly == 0 ? fwd::sparse_fwd_kernel<0>
             : poly == 2 ? fwd::sparse_fwd_kernel<2>

@@ -300,6 +300,12 @@ __device__ __forceinline__ uint64_t exp2_poly2(uint64_t x) {
   return (static_cast<uint64_t>(oh) << 32) | static_cast<uint64_t>(ol);
 }
 
+// Vector fp32 reduction into global memory (no return value).
+__device__ __forceinline__ void red_add_v4(float4* addr, float a, float b, float c, float d) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(a), "f"(b), "f"(c), "f"(d)
+               : "memory");
+}
+
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
