@@ -67,14 +67,13 @@ __device__ __forceinline__ uint32_t swz(uint32_t row, uint32_t chunk16) {
   return row * 128u + ((chunk16 ^ (row & 7u)) << 4);
 }
 
-// POLY: share of exponential pairs evaluated by the FMA-pipe polynomial
-// (0: none, 1: one pair in four, 2: one in eight, 3: one in two).
+// POLY: number of the 16 exponential pairs of a 32-column chunk evaluated by
+// the FMA-pipe polynomial instead of MUFU.EX2 (full tiles only; staircase
+// tiles, whose masked entries must be exactly 0, stay on MUFU). The chosen
+// pairs are spread evenly so ptxas can interleave them with the MUFU stream.
 template <int POLY>
-__device__ __forceinline__ bool use_poly(int c) {
-  if constexpr (POLY == 0) return false;
-  if constexpr (POLY == 1) return (c & 7) == 6;
-  if constexpr (POLY == 2) return (c & 15) == 14;
-  return (c & 7) >= 4;
+__device__ __forceinline__ constexpr bool use_poly(int pair) {
+  return POLY > 0 && ((pair * POLY) % 16) < POLY;
 }
 
 template <int POLY>
@@ -106,11 +105,26 @@ sparse_fwd_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constan
   const int32_t* selg = sel + (size_t)g * sel_stride;
   const int32_t* rows_t = rows + (size_t)h * N + row0;
 
+  // Softmax threads: row position, visible-key count and the Q row are
+  // fetched before the CTA barrier (the binary searches of all rows run in
+  // parallel); the thread owning a tile's last row publishes its key-tile count.
+  const int xs = (warp - 2) >> 2;                       // Q tile of a softmax warp
+  const int is = (warp & 3) * 32 + lane;                // its row == TMEM lane
+  const int nrows_s = min(BM, cnt - row0 - xs * BM);
+  const bool rvalid = warp >= 2 && is < nrows_s;
+  const int pos = rvalid ? __ldg(rows_t + xs * BM + is) : 0;
+  uint4 qv[16];
+  if (warp >= 2) {
+    const uint4* qrow = reinterpret_cast<const uint4*>(Q + ((size_t)h * N + pos) * D);
+#pragma unroll
+    for (int c = 0; c < 16; ++c) qv[c] = rvalid ? __ldg(qrow + c) : make_uint4(0, 0, 0, 0);
+  }
+  const int vis = rvalid ? count_le(selg, nsel, pos) : 0;
+  if (warp >= 2) {
+    if (is == nrows_s - 1) s_nt[xs] = (vis + BN - 1) / BN;
+    if (nrows_s <= 0 && is == 0) s_nt[xs] = 0;
+  }
   if (threadIdx.x == 0) {
-    for (int x = 0; x < 2; ++x) {
-      const int nr = min(BM, cnt - row0 - x * BM);
-      s_nt[x] = nr > 0 ? (count_le(selg, nsel, __ldg(rows_t + x * BM + nr - 1)) + BN - 1) / BN : 0;
-    }
     tma_prefetch_desc(&tm_k);
     tma_prefetch_desc(&tm_v);
     for (int x = 0; x < 2; ++x) {
@@ -157,19 +171,25 @@ sparse_fwd_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constan
     }
   } else if (warp == 1) {
     // ------------------------------------------------------ MMA issuer
-    if (lane == 0 && ntm > 0) {
+    // The whole warp runs the schedule (warp-uniform control and descriptor
+    // arithmetic in uniform registers); elect.sync picks the issuing lane.
+    if (ntm > 0) {
       constexpr uint32_t idesc_qk = idesc_bf16_f32(BM, BN, 0, 0);
       constexpr uint32_t idesc_pv = idesc_bf16_f32(BM, D, 0, 1);
       const int nt[2] = {ntA, ntB};
+      // Descriptor bases; per-K-step offsets are added to the 14-bit start
+      // address field (addresses < 256 KB, no carry out of the field).
+      const uint64_t dq0 = sdesc_sw128(sbase + OFF_Q, 16, 1024);
+      const uint64_t dk0 = sdesc_sw128(sbase + OFF_K, 16, 1024);
+      const uint64_t dv0 = sdesc_sw128(sbase + OFF_V, ATOM, 1024);
       auto qk = [&](int x, int j) {  // S_X(j) = Q_X K_j^T
-        const uint32_t qb = sbase + OFF_Q + x * TILE, kb = sbase + OFF_K + (j % NST) * TILE;
+        const uint64_t qd = dq0 + ((x * TILE) >> 4), kd = dk0 + (((j % NST) * TILE) >> 4);
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
-          const uint32_t off = (kk >> 2) * ATOM + (kk & 3) * 32;
-          umma_bf16(tmem + col_s(x), sdesc_sw128(qb + off, 16, 1024), sdesc_sw128(kb + off, 16, 1024), idesc_qk,
-                    kk > 0 ? 1u : 0u);
+          const uint32_t off = ((kk >> 2) * ATOM + (kk & 3) * 32) >> 4;
+          umma_bf16_ws(tmem + col_s(x), qd + off, kd + off, idesc_qk, kk > 0 ? 1u : 0u);
         }
-        umma_commit(B(B_SF + x));
+        umma_commit_ws(B(B_SF + x));
       };
       // prologue: S(0) for both tiles
       mbar_wait(B(B_KF), 0);
@@ -179,22 +199,21 @@ sparse_fwd_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constan
         tc_fence_after();
         qk(x, 0);
       }
-      umma_commit(B(B_KE + 0));
+      umma_commit_ws(B(B_KE + 0));
       for (int j = 0; j < ntm; ++j) {
         const int s = j % NST;
         mbar_wait(B(B_VF + s), (j / NST) & 1);
         bool kwaited = false;
+        const uint64_t vd = dv0 + ((s * TILE) >> 4);
         for (int x = 0; x < 2; ++x) {
           if (j >= nt[x]) continue;
           mbar_wait(B(B_PF + x), j & 1);  // P_X(j) written (and O_X corrected)
           tc_fence_after();
-          const uint32_t vb = sbase + OFF_V + s * TILE;
 #pragma unroll
-          for (int kk = 0; kk < 8; ++kk) {
-            const uint64_t b = sdesc_sw128(vb + kk * 2048, ATOM, 1024);
-            umma_bf16_ts(tmem + col_o(x), tmem + col_s(x) + kk * 8, b, idesc_pv, (j > 0 || kk > 0) ? 1u : 0u);
-          }
-          umma_commit(B(B_PV + x));
+          for (int kk = 0; kk < 8; ++kk)
+            umma_bf16_ts_ws(tmem + col_o(x), tmem + col_s(x) + kk * 8, vd + ((kk * 2048) >> 4), idesc_pv,
+                            (j > 0 || kk > 0) ? 1u : 0u);
+          umma_commit_ws(B(B_PV + x));
           if (j + 1 < nt[x]) {
             if (!kwaited) {
               mbar_wait(B(B_KF + (j + 1) % NST), ((j + 1) / NST) & 1);
@@ -204,55 +223,59 @@ sparse_fwd_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constan
             qk(x, j + 1);  // executes after PV_X(j): the tensor pipe is in order, so P is consumed first
           }
         }
-        umma_commit(B(B_VE + s));
-        if (kwaited) umma_commit(B(B_KE + (j + 1) % NST));
+        umma_commit_ws(B(B_VE + s));
+        if (kwaited) umma_commit_ws(B(B_KE + (j + 1) % NST));
       }
     }
   } else {
     // ------------------------------------------------------ softmax warps
-    const int x = (warp - 2) >> 2;               // Q tile of this warpgroup
+    const int x = xs;                            // Q tile of this warpgroup
     const int quarter = warp & 3;                // TMEM lane quarter of this warp
-    const int i = quarter * 32 + lane;           // row within the tile == TMEM lane
+    const int i = is;                            // row within the tile == TMEM lane
     const int nt = x ? ntB : ntA;
-    const int nrows = min(BM, cnt - row0 - x * BM);
-    const bool rvalid = i < nrows;
-    const int pos = rvalid ? __ldg(rows_t + x * BM + i) : 0;
-    const int vis = rvalid ? count_le(selg, nsel, pos) : 0;
     const uint32_t tl = tmem + ((uint32_t)(quarter * 32) << 16);
     float m_run = -INFINITY, l_run = 0.f;
     if (nt > 0) {
       // Q row -> swizzled K-major smem tile (A operand of S = Q K^T).
-      const uint4* qrow = reinterpret_cast<const uint4*>(Q + ((size_t)h * N + pos) * D);
       uint8_t* q_gen = smem + OFF_Q + x * TILE;
 #pragma unroll
-      for (int c = 0; c < 16; ++c) {
-        const uint4 v = rvalid ? __ldg(qrow + c) : make_uint4(0, 0, 0, 0);
-        *reinterpret_cast<uint4*>(q_gen + (c >> 3) * ATOM + swz(i, c & 7)) = v;
-      }
+      for (int c = 0; c < 16; ++c) *reinterpret_cast<uint4*>(q_gen + (c >> 3) * ATOM + swz(i, c & 7)) = qv[c];
       fence_proxy_async_smem();
       mbar_arrive(B(B_QF + x));
 
       const float sl2 = static_cast<float>(kLog2e / sqrt(static_cast<double>(D)));
+      const Exp2PolyConsts pc = exp2_poly_consts();
       for (int j = 0; j < nt; ++j) {
         mbar_wait(B(B_SF + x), j & 1);
         tc_fence_after();
+        if constexpr (POLY < 0) {  // profiling only: the MMA / TMA pipeline without softmax work
+          tc_fence_before();
+          mbar_arrive(B(B_PF + x));
+          l_run = 1.f;
+          continue;
+        }
         const int lim = vis - j * BN;
         const bool full = __all_sync(0xffffffffu, lim >= BN);
         // One pass over S in four 32-column TMEM chunks: raw row max and, when
         // `do_exp`, the exponentials against the current (possibly stale)
         // max, packed bf16 into pk[] and summed into the return value.
         uint32_t pk[64];
-        auto pass = [&](float nmu, bool do_exp, float& mt) -> float {
+        auto pass = [&](auto full_c, float nmu, bool do_exp, float& mt) -> float {
+          constexpr bool FULL = decltype(full_c)::value;
           const uint64_t c2 = f32x2(sl2, sl2), n2 = f32x2(nmu, nmu);
           uint64_t acc0 = f32x2(0.f, 0.f), acc1 = f32x2(0.f, 0.f);
           float m0 = -INFINITY, m1 = -INFINITY;
+          // Software-pipelined TMEM reads: chunk q+1 streams in while chunk
+          // q is reduced and exponentiated (two 32-column register buffers).
+          uint32_t sbuf[2][32];
+          __syncwarp();
+          tmem_ld32(tl + col_s(x), sbuf[0]);
+          tmem_wait_ld();
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
-            uint32_t sr[32];
-            __syncwarp();
-            tmem_ld32(tl + col_s(x) + q * 32, sr);
-            tmem_wait_ld();
-            if (!full) {  // staircase tile: masked keys -> -inf -> exactly 0
+            uint32_t* sr = sbuf[q & 1];
+            if (q < 3) tmem_ld32(tl + col_s(x) + (q + 1) * 32, sbuf[(q + 1) & 1]);
+            if constexpr (!FULL) {  // staircase tile: masked keys -> -inf -> exactly 0
 #pragma unroll
               for (int c = 0; c < 32; ++c)
                 if (q * 32 + c >= lim) sr[c] = __float_as_uint(-INFINITY);
@@ -267,14 +290,18 @@ sparse_fwd_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constan
               for (int c = 0; c < 32; c += 2) {
                 const uint64_t xx = ffma2(f32x2(__uint_as_float(sr[c]), __uint_as_float(sr[c + 1])), c2, n2);
                 uint64_t pp;
-                if (use_poly<POLY>(c)) {
-                  pp = exp2_poly2(xx);  // one pair in four on the FMA pipe (MUFU relief)
+                if (FULL && use_poly<POLY>(c >> 1)) {
+                  pp = exp2_poly_pair(xx, pc);  // FMA-pipe share (MUFU relief)
                 } else {
                   pp = f32x2(fast_exp2(f32x2_lo(xx)), fast_exp2(f32x2_hi(xx)));
                 }
                 if ((c & 2) == 0) acc0 = fadd2(acc0, pp); else acc1 = fadd2(acc1, pp);
                 pk[q * 16 + (c >> 1)] = pack_bf16x2(f32x2_lo(pp), f32x2_hi(pp));
               }
+            }
+            if (q < 3) {
+              tmem_wait_ld();
+              reg_fence32(sbuf[(q + 1) & 1]);
             }
           }
           mt = fmaxf(m0, m1);
@@ -289,7 +316,8 @@ sparse_fwd_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constan
         bool do_exp = !__any_sync(0xffffffffu, m_run == -INFINITY && lim > 0);
         for (int attempt = 0; attempt < 2; ++attempt) {
           float mt;
-          rsum = pass(m_run == -INFINITY ? 0.f : -m_run, do_exp, mt);
+          const float nmu = m_run == -INFINITY ? 0.f : -m_run;
+          rsum = full ? pass(std::true_type{}, nmu, do_exp, mt) : pass(std::false_type{}, nmu, do_exp, mt);
           if (attempt == 0) {
             const float m_new = fmaxf(m_run, mt * sl2);
             resc = m_new > m_run + 8.0f;
@@ -378,6 +406,8 @@ using namespace omni;
 int omni_make_tmap_rows(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols_elems, int elem_bytes,
                         uint32_t box_cols, uint32_t box_rows);
 
+static constexpr int kDefaultPoly = 6;
+
 extern "C" int omni_sparse_attn_fwd(const void* Q, const void* K_sel, const void* V_sel, const void* V,
                                     const int32_t* rows, const int32_t* counts, const int32_t* selected,
                                     const int32_t* sel_counts, int n_q_heads, int n_kv_heads, int seq_len,
@@ -392,22 +422,23 @@ extern "C" int omni_sparse_attn_fwd(const void* Q, const void* K_sel, const void
   if (st) return st;
   st = omni_make_tmap_rows(&tv, V_sel, (uint64_t)n_kv_heads * cap, 128, 2, 64, fwd::BN);
   if (st) return st;
-  // Tuning knob for the exp2 MUFU / FMA split (OMNI_FWD_POLY = 0..3). Default
-  // 0 (all MUFU): measured fastest on B200 at 64K (11.03 ms vs 11.19 / 11.58 /
-  // 12.71 ms for 1/8, 1/4, 1/2 polynomial; profiles/r01_fa_fwd_variants.json).
-  static int poly = [] {
+  // Tuning knob for the exp2 MUFU / FMA split: OMNI_FWD_POLY = number of the
+  // 16 exponential pairs per 32-column chunk on the FMA-pipe polynomial
+  // (0, 4, 6 or 8; full tiles only).
+  static const int poly = [] {
     const char* e = getenv("OMNI_FWD_POLY");
-    const int v = e ? atoi(e) : 0;
-    return (v >= 0 && v <= 3) ? v : 0;
+    const int v = e ? atoi(e) : kDefaultPoly;
+    return (v == -1 || v == 0 || v == 4 || v == 6 || v == 8) ? v : kDefaultPoly;
   }();
-  auto kern = poly == 0 ? fwd::sparse_fwd_kernel<0>
-            : poly == 2 ? fwd::sparse_fwd_kernel<2>
-            : poly == 3 ? fwd::sparse_fwd_kernel<3>
-                        : fwd::sparse_fwd_kernel<1>;
-  static bool attr_set[4] = {false, false, false, false};
-  if (!attr_set[poly]) {
+  auto kern = poly == -1 ? fwd::sparse_fwd_kernel<-1>  // profiling: MMA pipeline only, no softmax
+            : poly == 0 ? fwd::sparse_fwd_kernel<0>
+            : poly == 4 ? fwd::sparse_fwd_kernel<4>
+            : poly == 8 ? fwd::sparse_fwd_kernel<8>
+                        : fwd::sparse_fwd_kernel<6>;
+  static bool attr_set = false;
+  if (!attr_set) {
     OMNI_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fwd::SMEM_BYTES));
-    attr_set[poly] = true;
+    attr_set = true;
   }
   const int n_tiles = (seq_len + 2 * fwd::BM - 1) / (2 * fwd::BM);
   dim3 grid(n_tiles * n_q_heads);

@@ -13,6 +13,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
+#include <string.h>
+#include <type_traits>
 
 #include "../../include/omnisparse.h"
 
@@ -171,6 +173,17 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* r) {
       : "memory");
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+// Register fence for software-pipelined TMEM loads: after tcgen05.wait::ld,
+// route the destination registers of an in-flight tcgen05.ld through an empty
+// volatile asm so no consumer is scheduled above the wait.
+__device__ __forceinline__ void reg_fence32(uint32_t* r) {
+  asm volatile(""
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                 "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]),
+                 "+r"(r[15]), "+r"(r[16]), "+r"(r[17]), "+r"(r[18]), "+r"(r[19]), "+r"(r[20]), "+r"(r[21]),
+                 "+r"(r[22]), "+r"(r[23]), "+r"(r[24]), "+r"(r[25]), "+r"(r[26]), "+r"(r[27]), "+r"(r[28]),
+                 "+r"(r[29]), "+r"(r[30]), "+r"(r[31]));
+}
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 // --------------------------------------------------------------- tcgen05.mma
@@ -221,6 +234,37 @@ __device__ __forceinline__ void umma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, u
 // thread complete.
 __device__ __forceinline__ void umma_commit(uint32_t bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+
+// Warp-converged variants: the whole warp executes the call (so descriptor
+// arithmetic stays warp-uniform and lives in uniform registers) and
+// elect.sync picks the one lane that issues the tcgen05 instruction.
+__device__ __forceinline__ void umma_bf16_ws(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                             uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t.reg .b32 rx;\n\t"
+      "elect.sync rx|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void umma_bf16_ts_ws(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc,
+                                                uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t.reg .b32 rx;\n\t"
+      "elect.sync rx|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit_ws(uint32_t bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t.reg .b32 rx;\n\t"
+      "elect.sync rx|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(bar)
+      : "memory");
 }
 
 // --------------------------------------------------------------- misc math
@@ -298,6 +342,50 @@ __device__ __forceinline__ uint64_t exp2_poly2(uint64_t x) {
   const uint32_t pl = static_cast<uint32_t>(p), ph = static_cast<uint32_t>(p >> 32);
   const uint32_t ol = xl < -126.f ? 0u : pl + (rl << 23), oh = xh < -126.f ? 0u : ph + (rh << 23);
   return (static_cast<uint64_t>(oh) << 32) | static_cast<uint64_t>(ol);
+}
+
+// exp2 of a pair on the FMA/ALU pipes in 10 issue slots: clamp at -126,
+// round-to-nearest split x = n + f with the 1.5 * 2^23 magic constant,
+// degree-3 minimax polynomial for 2^f (max rel err 7.5e-5, far below the
+// bf16 rounding P receives), n added straight into the exponent field
+// ((bits(x + magic) << 23) == n << 23 mod 2^32). The caller guarantees no
+// masked (-inf) entries: for x < -126 the result is 2^-126-ish, not 0.
+struct Exp2PolyConsts {
+  uint64_t magic, c3, c2, c1, c0;
+};
+__host__ __device__ inline Exp2PolyConsts exp2_poly_consts() {
+  auto pr = [](float v) {
+    uint32_t b;
+    memcpy(&b, &v, 4);
+    return (static_cast<uint64_t>(b) << 32) | b;
+  };
+  return {pr(12582912.f), pr(0.05517165f), pr(0.24261116f), pr(0.69326099f), pr(0.99992807f)};
+}
+__device__ __forceinline__ uint64_t exp2_poly_pair(uint64_t x, const Exp2PolyConsts& k) {
+  uint64_t y;
+  asm("{\n\t"
+      ".reg .f32 xl, xh;\n\t"
+      ".reg .b64 xc, r, t, f, p;\n\t"
+      ".reg .b32 rl, rh, pl, ph;\n\t"
+      "mov.b64 {xl, xh}, %1;\n\t"
+      "max.f32 xl, xl, 0fC2FC0000;\n\t"
+      "max.f32 xh, xh, 0fC2FC0000;\n\t"
+      "mov.b64 xc, {xl, xh};\n\t"
+      "add.rn.f32x2 r, xc, %2;\n\t"
+      "sub.rn.f32x2 t, r, %2;\n\t"
+      "sub.rn.f32x2 f, xc, t;\n\t"
+      "fma.rn.f32x2 p, f, %3, %4;\n\t"
+      "fma.rn.f32x2 p, p, f, %5;\n\t"
+      "fma.rn.f32x2 p, p, f, %6;\n\t"
+      "mov.b64 {rl, rh}, r;\n\t"
+      "mov.b64 {pl, ph}, p;\n\t"
+      "mad.lo.u32 pl, rl, 8388608, pl;\n\t"
+      "mad.lo.u32 ph, rh, 8388608, ph;\n\t"
+      "mov.b64 %0, {pl, ph};\n\t"
+      "}"
+      : "=l"(y)
+      : "l"(x), "l"(k.magic), "l"(k.c3), "l"(k.c2), "l"(k.c1), "l"(k.c0));
+  return y;
 }
 
 // Vector fp32 reduction into global memory (no return value).

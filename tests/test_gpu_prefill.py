@@ -198,7 +198,13 @@ def test_exact_score_source_matches_reference_fixture(golden, tag, gran):
     active, mass, sel = out[3], out[8], out[9]
     torch.cuda.synchronize()
     np.testing.assert_array_equal(active.cpu().numpy().astype(bool), g[f"{tag}_active"])
-    np.testing.assert_allclose(mass.cpu().numpy(), g[f"{tag}_scores"], rtol=1e-10, atol=1e-13)
+    # The fixture ran on the unrounded float64 workload; the GPU consumes the
+    # fp32-rounded copy, so the masses agree to fp32 input rounding (~1e-7)
+    # with the fixture and to 1e-10 with the oracle on the rounded inputs.
+    np.testing.assert_allclose(mass.cpu().numpy(), g[f"{tag}_scores"], rtol=1e-6, atol=1e-12)
+    Qr, Kr = [x.astype(np.float32).astype(np.float64) for x in (Q, K)]
+    ref = opipe.select(Qr, Kr, 120, 0, 0.08, 0.82, 16, granularity=gran, score_source="exact")
+    np.testing.assert_allclose(mass.cpu().numpy(), np.stack(ref.group_scores), rtol=1e-10, atol=1e-13)
     b = int(sel.info[0])
     assert b == int(g[f"{tag}_budget"]) and int(sel.info[1]) == int(g[f"{tag}_flattest"])
     np.testing.assert_array_equal(sel.selected[:, :b].cpu().numpy(), g[f"{tag}_selected"])
