@@ -14,19 +14,23 @@
 //   O += P V  : A = P (TMEM, bf16 pairs written over S),  B = V (smem)
 // TMEM per tile X: S/P columns [256X, 256X+128), O [256X+128, 256X+256).
 //
-// Warp roles (320 threads, 1 CTA / SM, ~193 KB smem, 512 TMEM columns):
+// Warp roles (576 threads, 1 CTA / SM, ~197 KB smem, 512 TMEM columns):
 //   warp 0      TMA producer: K_j, V_j (two 64-column SWIZZLE_128B boxes each)
 //               into 2-stage rings.
 //   warp 1      TMEM allocator + single-thread tcgen05.mma issuer, ping-pong
 //               per key tile j: PV_A(j), QK_A(j+1), PV_B(j), QK_B(j+1) — the
 //               tensor core runs one tile's GEMMs while the other tile's
 //               softmax warps work.
-//   warps 2-5   softmax / correction / epilogue of tile A, warps 6-9 of tile
-//               B; thread <-> row <-> TMEM lane (warp % 4 selects the lane
-//               quarter). Full row per thread (no cross-warp exchange),
-//               exp2-domain online softmax with lazy rescaling (O corrected
-//               only when the running max grows by more than 2^8), a quarter
-//               of the exponentials on the FMA pipe.
+//   warps 2-17  softmax / correction / epilogue: warps 2-9 own tile A, 10-17
+//               tile B. Two warps per TMEM lane quarter and tile split the 128
+//               key columns (64 each), so every row is served by two threads
+//               in different warps: the per-tile softmax latency, which bounds
+//               the ping-pong (S -> P -> PV/QK -> S), is halved while the issue
+//               slots of each SM sub-partition are shared by four softmax
+//               warps. Row maxima are exchanged through shared memory with a
+//               64-thread named barrier per (tile, lane quarter); exp2-domain
+//               online softmax with lazy rescaling (O corrected only when the
+//               running max grows by more than 2^8).
 // Epilogue: O / l -> bf16 rows scattered to their original positions; rows
 // with no visible key copy V[g, sink] (prefill.py:119-120); LSE side output
 // for the backward kernel.
@@ -39,6 +43,8 @@ namespace omni {
 namespace fwd {
 
 constexpr int BM = 128, BN = 128, D = 128, NST = 2;
+constexpr int NTHREADS = 576;  // TMA warp + MMA warp + 16 softmax warps
+constexpr int HC = 64;         // key columns per softmax thread (half a tile row)
 constexpr uint32_t ATOM = 128 * 128;  // 128 rows x 128 B swizzle region
 constexpr uint32_t TILE = 2 * ATOM;   // 128 x 128 bf16
 constexpr uint32_t OFF_Q = 0;                     // 2 Q tiles
@@ -76,8 +82,12 @@ __device__ __forceinline__ constexpr bool use_poly(int pair) {
   return POLY > 0 && ((pair * POLY) % 16) < POLY;
 }
 
-template <int POLY>
-__global__ void __launch_bounds__(320, 1)
+// Profiling-only cycle accounting (OMNI_FWD_TRACE=1): per-phase clock sums of
+// lane 0 of every softmax / MMA warp, read back with omni_debug_fwd_trace.
+__device__ unsigned long long g_fwd_trace[8];
+
+template <int POLY, bool TRACE = false>
+__global__ void __launch_bounds__(NTHREADS, 1)
 sparse_fwd_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
                   const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __restrict__ Vorig,
                   const int32_t* __restrict__ rows, const int32_t* __restrict__ counts,
@@ -98,6 +108,7 @@ sparse_fwd_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constan
   auto B = [&](int i) { return bar + 8u * i; };
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + OFF_TMEM);
   __shared__ int s_nt[2];
+  __shared__ float s_xch[2][BM][2];  // per (tile, row, half): partial row max, then l
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = h / rep;
@@ -105,22 +116,24 @@ sparse_fwd_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constan
   const int32_t* selg = sel + (size_t)g * sel_stride;
   const int32_t* rows_t = rows + (size_t)h * N + row0;
 
-  // Softmax threads: row position, visible-key count and the Q row are
-  // fetched before the CTA barrier (the binary searches of all rows run in
+  // Softmax threads: row position, visible-key count and the Q half-row
+  // are fetched before the CTA barrier (the binary searches of all rows run in
   // parallel); the thread owning a tile's last row publishes its key-tile count.
-  const int xs = (warp - 2) >> 2;                       // Q tile of a softmax warp
+  const int sidx = warp - 2;                            // softmax warp index 0..15
+  const int xs = sidx >> 3;                             // its Q tile
+  const int hf = (sidx >> 2) & 1;                       // its key-column half
   const int is = (warp & 3) * 32 + lane;                // its row == TMEM lane
   const int nrows_s = min(BM, cnt - row0 - xs * BM);
   const bool rvalid = warp >= 2 && is < nrows_s;
   const int pos = rvalid ? __ldg(rows_t + xs * BM + is) : 0;
-  uint4 qv[16];
+  uint4 qv[8];
   if (warp >= 2) {
-    const uint4* qrow = reinterpret_cast<const uint4*>(Q + ((size_t)h * N + pos) * D);
+    const uint4* qrow = reinterpret_cast<const uint4*>(Q + ((size_t)h * N + pos) * D) + hf * 8;
 #pragma unroll
-    for (int c = 0; c < 16; ++c) qv[c] = rvalid ? __ldg(qrow + c) : make_uint4(0, 0, 0, 0);
+    for (int c = 0; c < 8; ++c) qv[c] = rvalid ? __ldg(qrow + c) : make_uint4(0, 0, 0, 0);
   }
   const int vis = rvalid ? count_le(selg, nsel, pos) : 0;
-  if (warp >= 2) {
+  if (warp >= 2 && hf == 0) {
     if (is == nrows_s - 1) s_nt[xs] = (vis + BN - 1) / BN;
     if (nrows_s <= 0 && is == 0) s_nt[xs] = 0;
   }
@@ -128,9 +141,9 @@ sparse_fwd_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constan
     tma_prefetch_desc(&tm_k);
     tma_prefetch_desc(&tm_v);
     for (int x = 0; x < 2; ++x) {
-      mbar_init(B(B_QF + x), 128);
+      mbar_init(B(B_QF + x), 2 * BM);
       mbar_init(B(B_SF + x), 1);
-      mbar_init(B(B_PF + x), 128);
+      mbar_init(B(B_PF + x), 2 * BM);
       mbar_init(B(B_PV + x), 1);
     }
     for (int s = 0; s < NST; ++s) {
@@ -207,11 +220,17 @@ sparse_fwd_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constan
         const uint64_t vd = dv0 + ((s * TILE) >> 4);
         for (int x = 0; x < 2; ++x) {
           if (j >= nt[x]) continue;
-          mbar_wait(B(B_PF + x), j & 1);  // P_X(j) written (and O_X corrected)
+          if constexpr (TRACE) {
+            const uint32_t t0 = clock();
+            mbar_wait(B(B_PF + x), j & 1);
+            if (lane == 0) atomicAdd(&g_fwd_trace[6], (unsigned long long)(clock() - t0));
+          } else {
+            mbar_wait(B(B_PF + x), j & 1);  // P_X(j) written (and O_X corrected)
+          }
           tc_fence_after();
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk)
-            umma_bf16_ts_ws(tmem + col_o(x), tmem + col_s(x) + kk * 8, vd + ((kk * 2048) >> 4), idesc_pv,
+            umma_bf16_ts_ws(tmem + col_o(x), tmem + col_s(x) + (kk >> 2) * HC + (kk & 3) * 8, vd + ((kk * 2048) >> 4), idesc_pv,
                             (j > 0 || kk > 0) ? 1u : 0u);
           umma_commit_ws(B(B_PV + x));
           if (j + 1 < nt[x]) {
@@ -229,144 +248,183 @@ sparse_fwd_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constan
     }
   } else {
     // ------------------------------------------------------ softmax warps
-    const int x = xs;                            // Q tile of this warpgroup
+    const int x = xs;                            // Q tile of this warp
     const int quarter = warp & 3;                // TMEM lane quarter of this warp
     const int i = is;                            // row within the tile == TMEM lane
+    const int cb = hf * HC;                      // first key column of this thread
+    const uint32_t bid = 1 + x * 4 + quarter;    // named barrier of the two halves of these rows
     const int nt = x ? ntB : ntA;
     const uint32_t tl = tmem + ((uint32_t)(quarter * 32) << 16);
     float m_run = -INFINITY, l_run = 0.f;
     if (nt > 0) {
-      // Q row -> swizzled K-major smem tile (A operand of S = Q K^T).
-      uint8_t* q_gen = smem + OFF_Q + x * TILE;
+      // Q half-row -> swizzled K-major smem tile (A operand of S = Q K^T).
+      uint8_t* q_gen = smem + OFF_Q + x * TILE + hf * ATOM;
 #pragma unroll
-      for (int c = 0; c < 16; ++c) *reinterpret_cast<uint4*>(q_gen + (c >> 3) * ATOM + swz(i, c & 7)) = qv[c];
+      for (int c = 0; c < 8; ++c) *reinterpret_cast<uint4*>(q_gen + swz(i, c)) = qv[c];
       fence_proxy_async_smem();
       mbar_arrive(B(B_QF + x));
 
       const float sl2 = static_cast<float>(kLog2e / sqrt(static_cast<double>(D)));
       const Exp2PolyConsts pc = exp2_poly_consts();
+      uint32_t tr[5] = {0, 0, 0, 0, 0};
+      uint32_t tc0 = clock();
+      auto tick = [&](int k) {
+        if constexpr (TRACE) {
+          const uint32_t t = clock();
+          tr[k] += t - tc0;
+          tc0 = t;
+        }
+      };
       for (int j = 0; j < nt; ++j) {
-        mbar_wait(B(B_SF + x), j & 1);
+        tick(4);
+        mbar_wait(B(B_SF + x), j & 1);  // S_X(j) ready (and, in order, PV_X(j-1) done)
         tc_fence_after();
+        tick(0);
         if constexpr (POLY < 0) {  // profiling only: the MMA / TMA pipeline without softmax work
           tc_fence_before();
           mbar_arrive(B(B_PF + x));
           l_run = 1.f;
           continue;
         }
-        const int lim = vis - j * BN;
-        const bool full = __all_sync(0xffffffffu, lim >= BN);
-        // One pass over S in four 32-column TMEM chunks: raw row max and, when
-        // `do_exp`, the exponentials against the current (possibly stale)
-        // max, packed bf16 into pk[] and summed into the return value.
-        uint32_t pk[64];
-        auto pass = [&](auto full_c, float nmu, bool do_exp, float& mt) -> float {
+        const int lim_row = vis - j * BN;  // visible keys of this row in key tile j
+        const int lim = lim_row - cb;      // ... within this thread's 64 columns
+        const bool full = __all_sync(0xffffffffu, lim >= HC);
+        // exp2(s * sl2 - m) of a 32-column chunk -> packed bf16 pk[16], row sum
+        auto exps = [&](auto full_c, const uint32_t* sr, float nmu, uint32_t* pk) -> float {
           constexpr bool FULL = decltype(full_c)::value;
           const uint64_t c2 = f32x2(sl2, sl2), n2 = f32x2(nmu, nmu);
           uint64_t acc0 = f32x2(0.f, 0.f), acc1 = f32x2(0.f, 0.f);
-          float m0 = -INFINITY, m1 = -INFINITY;
-          // Software-pipelined TMEM reads: chunk q+1 streams in while chunk
-          // q is reduced and exponentiated (two 32-column register buffers).
-          uint32_t sbuf[2][32];
-          __syncwarp();
-          tmem_ld32(tl + col_s(x), sbuf[0]);
-          tmem_wait_ld();
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            uint32_t* sr = sbuf[q & 1];
-            if (q < 3) tmem_ld32(tl + col_s(x) + (q + 1) * 32, sbuf[(q + 1) & 1]);
-            if constexpr (!FULL) {  // staircase tile: masked keys -> -inf -> exactly 0
-#pragma unroll
-              for (int c = 0; c < 32; ++c)
-                if (q * 32 + c >= lim) sr[c] = __float_as_uint(-INFINITY);
+          for (int c = 0; c < 32; c += 2) {
+            const uint64_t xx = ffma2(f32x2(__uint_as_float(sr[c]), __uint_as_float(sr[c + 1])), c2, n2);
+            uint64_t pp;
+            if (FULL && use_poly<POLY>(c >> 1)) {
+              pp = exp2_poly_pair(xx, pc);  // FMA-pipe share (MUFU relief)
+            } else {
+              pp = f32x2(fast_exp2(f32x2_lo(xx)), fast_exp2(f32x2_hi(xx)));
             }
-#pragma unroll
-            for (int c = 0; c < 32; c += 4) {
-              m0 = fmax3(m0, __uint_as_float(sr[c]), __uint_as_float(sr[c + 1]));
-              m1 = fmax3(m1, __uint_as_float(sr[c + 2]), __uint_as_float(sr[c + 3]));
-            }
-            if (do_exp) {
-#pragma unroll
-              for (int c = 0; c < 32; c += 2) {
-                const uint64_t xx = ffma2(f32x2(__uint_as_float(sr[c]), __uint_as_float(sr[c + 1])), c2, n2);
-                uint64_t pp;
-                if (FULL && use_poly<POLY>(c >> 1)) {
-                  pp = exp2_poly_pair(xx, pc);  // FMA-pipe share (MUFU relief)
-                } else {
-                  pp = f32x2(fast_exp2(f32x2_lo(xx)), fast_exp2(f32x2_hi(xx)));
-                }
-                if ((c & 2) == 0) acc0 = fadd2(acc0, pp); else acc1 = fadd2(acc1, pp);
-                pk[q * 16 + (c >> 1)] = pack_bf16x2(f32x2_lo(pp), f32x2_hi(pp));
-              }
-            }
-            if (q < 3) {
-              tmem_wait_ld();
-              reg_fence32(sbuf[(q + 1) & 1]);
-            }
+            if ((c & 2) == 0) acc0 = fadd2(acc0, pp); else acc1 = fadd2(acc1, pp);
+            pk[c >> 1] = pack_bf16x2(f32x2_lo(pp), f32x2_hi(pp));
           }
-          mt = fmaxf(m0, m1);
           const uint64_t acc = fadd2(acc0, acc1);
           return f32x2_lo(acc) + f32x2_hi(acc);
         };
-        // Speculate with the running max (no separate max pass); redo the
-        // tile only when some row's max grew by more than 2^8 (lazy rescale).
-        float rsum = 0.f, alpha = 1.f;
-        bool resc = false;
-        // a row seeing its first visible keys has no max to speculate with
-        bool do_exp = !__any_sync(0xffffffffu, m_run == -INFINITY && lim > 0);
-        for (int attempt = 0; attempt < 2; ++attempt) {
-          float mt;
-          const float nmu = m_run == -INFINITY ? 0.f : -m_run;
-          rsum = full ? pass(std::true_type{}, nmu, do_exp, mt) : pass(std::false_type{}, nmu, do_exp, mt);
-          if (attempt == 0) {
-            const float m_new = fmaxf(m_run, mt * sl2);
-            resc = m_new > m_run + 8.0f;
-            if (resc) {
-              alpha = (m_run == -INFINITY) ? 0.f : fast_exp2(m_run - m_new);
-              m_run = m_new;
-            }
-          }
-          if (do_exp && !__any_sync(0xffffffffu, attempt == 0 && resc)) break;
-          do_exp = true;
-        }
-
-        if (j > 0) {
-          mbar_wait(B(B_PV + x), (j - 1) & 1);  // PV_X(j-1) done: O stable
-          tc_fence_after();
-          if (__any_sync(0xffffffffu, resc)) {
+        // The running max m_run (log2 domain) is integral and shared by both
+        // halves of a row. Chunks are exponentiated optimistically against
+        // the current max m_cur while the chunk max is reduced alongside (no
+        // max -> exp dependency); only a chunk exceeding m_cur by more than
+        // 2^64 (the first visible tile, or an extreme logit jump) is redone
+        // from registers against ceil(chunk max), so P <= 2^64 always.
+        // Growth beyond 2^8 is settled after both chunks: one OR-barrier
+        // between the halves; on the (rare) true branch they exchange their
+        // maxima and rescale P, l and O by exact powers of two.
+        auto chunk = [&](int q, float& m_cur, float& cmax, float& mu) -> float {
+          uint32_t sr[32], pk[16];
+          __syncwarp();
+          tmem_ld32(tl + col_s(x) + cb + q * 32, sr);
+          tmem_wait_ld();
+          if (!full) {  // staircase tile: masked keys -> -inf -> exactly 0
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
+            for (int c = 0; c < 32; ++c)
+              if (q * 32 + c >= lim) sr[c] = __float_as_uint(-INFINITY);
+          }
+          float m0 = -INFINITY, m1 = -INFINITY;
+#pragma unroll
+          for (int c = 0; c < 32; c += 4) {
+            m0 = fmax3(m0, __uint_as_float(sr[c]), __uint_as_float(sr[c + 1]));
+            m1 = fmax3(m1, __uint_as_float(sr[c + 2]), __uint_as_float(sr[c + 3]));
+          }
+          float rs = full ? exps(std::true_type{}, sr, m_cur == -INFINITY ? 0.f : -m_cur, pk)
+                          : exps(std::false_type{}, sr, m_cur == -INFINITY ? 0.f : -m_cur, pk);
+          const float cm = fmaxf(m0, m1) * sl2;
+          cmax = fmaxf(cmax, cm);
+          const bool hard = cm > m_cur + 64.0f;
+          if (__any_sync(0xffffffffu, hard)) {
+            if (hard) m_cur = ceilf(cm);
+            rs = full ? exps(std::true_type{}, sr, m_cur == -INFINITY ? 0.f : -m_cur, pk)
+                      : exps(std::false_type{}, sr, m_cur == -INFINITY ? 0.f : -m_cur, pk);
+          }
+          mu = m_cur;
+          tmem_st16(tl + col_s(x) + cb + q * 16, pk);  // P over this thread's own, already-read S columns
+          return rs;
+        };
+        float m_cur = m_run, cmax = -INFINITY, mu0, mu1;
+        const float rs0 = chunk(0, m_cur, cmax, mu0);
+        tick(1);
+        const float rs1 = chunk(1, m_cur, cmax, mu1);
+        tick(2);
+        // target max of this half: its P max, raised when the tile grew > 2^8
+        const float tgt = cmax > mu1 + 8.0f ? ceilf(cmax) : mu1;
+        if (named_bar_red_or(bid, 2 * 32, tgt != m_run)) {
+          s_xch[x][i][hf] = tgt;
+          named_bar_sync(bid, 2 * 32);
+          const float m_fin = fmaxf(tgt, s_xch[x][i][hf ^ 1]);
+          named_bar_sync(bid, 2 * 32);  // both read before the slots are reused
+          float f0 = 1.f, f1 = 1.f, alpha = 1.f;
+          if (m_fin != -INFINITY) {
+            f0 = pow2_int(mu0 - m_fin);
+            f1 = pow2_int(mu1 - m_fin);
+            alpha = pow2_int(m_run - m_fin);
+          }
+          l_run = l_run * alpha + rs0 * f0 + rs1 * f1;
+          m_run = m_fin;
+          if (__any_sync(0xffffffffu, f0 != 1.f)) {  // (f1 != 1 implies f0 != 1)
+            uint32_t pw[32];
+            tmem_wait_st();
+            __syncwarp();
+            tmem_ld32(tl + col_s(x) + cb, pw);
+            tmem_wait_ld();
+            const uint32_t a0 = pack_bf16x2(f0, f0), a1 = pack_bf16x2(f1, f1);
+#pragma unroll
+            for (int c = 0; c < 16; ++c) pw[c] = mul_bf16x2(pw[c], a0);
+#pragma unroll
+            for (int c = 16; c < 32; ++c) pw[c] = mul_bf16x2(pw[c], a1);
+            tmem_st32(tl + col_s(x) + cb, pw);
+          }
+          if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
+            // O_X(j-1) is stable: PV_X(j-1) precedes QK_X(j) in the tensor pipe
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
               uint32_t o[32];
               __syncwarp();
-              tmem_ld32(tl + col_o(x) + q * 32, o);
+              tmem_ld32(tl + col_o(x) + cb + q * 32, o);
               tmem_wait_ld();
 #pragma unroll
               for (int c = 0; c < 32; ++c) o[c] = __float_as_uint(__uint_as_float(o[c]) * alpha);
-              tmem_st32(tl + col_o(x) + q * 32, o);
+              tmem_st32(tl + col_o(x) + cb + q * 32, o);
             }
           }
+        } else {
+          l_run += rs0 + rs1;
         }
-        // P (bf16 pairs) over S columns [0, 64): the A operand of PV_X(j).
-        __syncwarp();
-#pragma unroll
-        for (int q = 0; q < 4; ++q) tmem_st16(tl + col_s(x) + q * 16, pk + q * 16);
-        l_run = l_run * alpha + rsum;
+        tick(3);
         tmem_wait_st();
         tc_fence_before();
         mbar_arrive(B(B_PF + x));
       }
+      tick(4);
+      if constexpr (TRACE) {
+        if (lane == 0) {
+          for (int k = 0; k < 5; ++k) atomicAdd(&g_fwd_trace[k], (unsigned long long)tr[k]);
+          atomicAdd(&g_fwd_trace[5], (unsigned long long)nt);
+        }
+      }
       mbar_wait(B(B_PV + x), (nt - 1) & 1);
       tc_fence_after();
+      // the row normaliser is the sum of both halves' partial sums
+      s_xch[x][i][hf] = l_run;
+      named_bar_sync(bid, 2 * 32);
+      l_run += s_xch[x][i][hf ^ 1];
     }
     // ------------------------------------------------------ epilogue
-    uint4* dst = reinterpret_cast<uint4*>(O + ((size_t)h * N + pos) * D);
+    uint4* dst = reinterpret_cast<uint4*>(O + ((size_t)h * N + pos) * D + cb);
     if (nt > 0) {
       const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < 2; ++q) {
         uint32_t o[32];
         __syncwarp();
-        tmem_ld32(tl + col_o(x) + q * 32, o);
+        tmem_ld32(tl + col_o(x) + cb + q * 32, o);
         tmem_wait_ld();
         if (rvalid && l_run > 0.f) {
 #pragma unroll
@@ -380,12 +438,12 @@ sparse_fwd_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constan
     }
     if (rvalid) {
       if (l_run > 0.f) {
-        if (lse) lse[(size_t)h * N + pos] = static_cast<float>(M_LN2) * (m_run + log2f(l_run));
+        if (lse && hf == 0) lse[(size_t)h * N + pos] = static_cast<float>(M_LN2) * (m_run + log2f(l_run));
       } else {
-        const uint4* src = reinterpret_cast<const uint4*>(Vorig + ((size_t)g * N + sink) * D);
+        const uint4* src = reinterpret_cast<const uint4*>(Vorig + ((size_t)g * N + sink) * D + cb);
 #pragma unroll
-        for (int c = 0; c < 16; ++c) dst[c] = __ldg(src + c);
-        if (lse) lse[(size_t)h * N + pos] = -INFINITY;
+        for (int c = 0; c < 8; ++c) dst[c] = __ldg(src + c);
+        if (lse && hf == 0) lse[(size_t)h * N + pos] = -INFINITY;
       }
     }
   }
@@ -406,7 +464,7 @@ using namespace omni;
 int omni_make_tmap_rows(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols_elems, int elem_bytes,
                         uint32_t box_cols, uint32_t box_rows);
 
-static constexpr int kDefaultPoly = 6;
+static constexpr int kDefaultPoly = 4;
 
 extern "C" int omni_sparse_attn_fwd(const void* Q, const void* K_sel, const void* V_sel, const void* V,
                                     const int32_t* rows, const int32_t* counts, const int32_t* selected,
@@ -430,7 +488,12 @@ extern "C" int omni_sparse_attn_fwd(const void* Q, const void* K_sel, const void
     const int v = e ? atoi(e) : kDefaultPoly;
     return (v == -1 || v == 0 || v == 4 || v == 6 || v == 8) ? v : kDefaultPoly;
   }();
-  auto kern = poly == -1 ? fwd::sparse_fwd_kernel<-1>  // profiling: MMA pipeline only, no softmax
+  static const bool trace = [] {
+    const char* e = getenv("OMNI_FWD_TRACE");
+    return e && atoi(e) != 0;
+  }();
+  auto kern = trace ? fwd::sparse_fwd_kernel<4, true>  // profiling: per-phase cycle accounting
+            : poly == -1 ? fwd::sparse_fwd_kernel<-1>  // profiling: MMA pipeline only, no softmax
             : poly == 0 ? fwd::sparse_fwd_kernel<0>
             : poly == 4 ? fwd::sparse_fwd_kernel<4>
             : poly == 8 ? fwd::sparse_fwd_kernel<8>
@@ -442,9 +505,18 @@ extern "C" int omni_sparse_attn_fwd(const void* Q, const void* K_sel, const void
   }
   const int n_tiles = (seq_len + 2 * fwd::BM - 1) / (2 * fwd::BM);
   dim3 grid(n_tiles * n_q_heads);
-  kern<<<grid, 320, fwd::SMEM_BYTES, static_cast<cudaStream_t>(stream)>>>(
+  kern<<<grid, fwd::NTHREADS, fwd::SMEM_BYTES, static_cast<cudaStream_t>(stream)>>>(
       tk, tv, static_cast<const __nv_bfloat16*>(Q), static_cast<const __nv_bfloat16*>(V), rows, counts, selected,
       sel_counts, n_q_heads, n_q_heads / n_kv_heads, seq_len, cap, seq_len, sink_index, n_tiles,
       static_cast<__nv_bfloat16*>(O), lse);
   return omni_launch_check();
+}
+
+// Profiling support (OMNI_FWD_TRACE=1): copies the 8 per-phase cycle sums
+// of the traced K4 launches to host memory and resets them.
+extern "C" int omni_debug_fwd_trace(unsigned long long* host8) {
+  OMNI_CUDA_TRY(cudaMemcpyFromSymbol(host8, fwd::g_fwd_trace, sizeof(unsigned long long) * 8));
+  unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  OMNI_CUDA_TRY(cudaMemcpyToSymbol(fwd::g_fwd_trace, z, sizeof(z)));
+  return OMNI_OK;
 }
