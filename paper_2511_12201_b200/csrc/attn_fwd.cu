@@ -36,6 +36,7 @@
 // for the backward kernel.
 #include <math.h>
 #include <stdlib.h>
+#include <string.h>
 
 #include "common.cuh"
 
@@ -466,6 +467,11 @@ int omni_make_tmap_rows(CUtensorMap* map, const void* base, uint64_t rows, uint6
 
 static constexpr int kDefaultPoly = 4;
 
+int omni_sparse_attn_fwd_pair(const void* Q, const void* K_sel, const void* V_sel, const void* V, const int32_t* rows,
+                              const int32_t* counts, const int32_t* selected, const int32_t* sel_counts,
+                              int n_q_heads, int n_kv_heads, int seq_len, int cap, int sink_index, void* O,
+                              float* lse, int poly, cudaStream_t stream);
+
 extern "C" int omni_sparse_attn_fwd(const void* Q, const void* K_sel, const void* V_sel, const void* V,
                                     const int32_t* rows, const int32_t* counts, const int32_t* selected,
                                     const int32_t* sel_counts, int n_q_heads, int n_kv_heads, int seq_len,
@@ -475,6 +481,22 @@ extern "C" int omni_sparse_attn_fwd(const void* Q, const void* K_sel, const void
   OMNI_CHECK(cap >= 128 && cap % 128 == 0, OMNI_E_SHAPE, "cap must be a positive multiple of 128");
   OMNI_CHECK(sink_index >= 0 && sink_index < seq_len, OMNI_E_LAYOUT, "sink_index outside the sequence");
   OMNI_CHECK(seq_len >= 1, OMNI_E_SHAPE, "empty sequence");
+  // Kernel choice: the single-CTA two-Q-tile ping-pong kernel below by
+  // default (measured fastest: 10.0 ms vs 11.0 ms at the 64K bench workload);
+  // OMNI_FWD_IMPL=pair selects the CTA-pair kernel of attn_fwd2.cu (faster
+  // MMA/TMA pipeline, 6.8 vs 7.2 ms without softmax work, but its one-tile-per-SM
+  // softmax is the bottleneck; profiles/r01_k4_notes.md).
+  static const bool single = [] {
+    const char* e = getenv("OMNI_FWD_IMPL");
+    return !(e && strcmp(e, "pair") == 0);
+  }();
+  static const int poly_env = [] {
+    const char* e = getenv("OMNI_FWD_POLY");
+    return e ? atoi(e) : kDefaultPoly;
+  }();
+  if (!single)
+    return omni_sparse_attn_fwd_pair(Q, K_sel, V_sel, V, rows, counts, selected, sel_counts, n_q_heads, n_kv_heads,
+                                     seq_len, cap, sink_index, O, lse, poly_env, static_cast<cudaStream_t>(stream));
   CUtensorMap tk, tv;
   int st = omni_make_tmap_rows(&tk, K_sel, (uint64_t)n_kv_heads * cap, 128, 2, 64, fwd::BN);
   if (st) return st;

@@ -1,0 +1,52 @@
+"""K4 kernel variants (selected once per process by environment variables)
+against the oracle: the single-CTA ping-pong kernel at several MUFU / FMA-pipe
+exp2 splits and the CTA-pair (cta_group::2) kernel. Each variant runs in its
+own subprocess on a GQA workload with ragged N (partial tiles, staircase)."""
+
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+CODE = r"""
+import json, sys
+import numpy as np, torch
+sys.path.insert(0, ".")
+from oracle import attention as oatt
+from oracle import pipeline as opipe
+from oracle.workload import Spec, generate, round_bf16
+from paper_2511_12201_b200.pipeline import SparsityConfig, sparse_prefill_device
+Q, K, V = generate(Spec(heads=8, heads_kv=2, head_dim=128, n_vision=4999, n_text=77, seed=3))
+Q, K, V = round_bf16(Q), round_bf16(K), round_bf16(V)
+t = lambda x: torch.tensor(x, dtype=torch.bfloat16, device="cuda")
+res = sparse_prefill_device(t(Q), t(K), t(V), 4999, SparsityConfig())
+torch.cuda.synchronize()
+ref = opipe.select(Q, K, 4999, 0, 0.08, 0.82, 256)
+out = res.outputs.float().cpu().numpy()
+lse = res.lse.cpu().numpy()
+err = 0.0
+for h in (0, 3, 4, 7):
+    g = h // 4
+    exp = oatt.sparse_head_attention(Q[h], K[g], V[g], ref.selected[g], ref.active[h], 0)
+    err = max(err, float(np.max(np.abs(out[h] - exp) / (0.02 + 0.02 * np.abs(exp)))))
+    act = np.flatnonzero(ref.active[h])
+    el = oatt.sparse_head_lse(Q[h], K[g], ref.selected[g], ref.active[h])
+    fin = np.isfinite(el[act])
+    err = max(err, float(np.max(np.abs(lse[h][act][fin] - el[act][fin]))) / 0.02)
+print(json.dumps({"scaled_err": err, "nan": bool(np.isnan(out).any())}))
+"""
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("impl,poly", [("single", "0"), ("single", "4"), ("single", "8"), ("pair", "0"), ("pair", "4")])
+def test_forward_variant_matches_oracle(impl, poly):
+    env = dict(os.environ, OMNI_FWD_IMPL=impl, OMNI_FWD_POLY=poly)
+    out = subprocess.run([sys.executable, "-c", CODE], cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    r = json.loads(out.stdout.strip().splitlines()[-1])
+    assert not r["nan"]
+    assert r["scaled_err"] <= 1.0, r  # |err| <= 0.02 + 0.02 |ref| (bf16 P, fp32 accumulation)
