@@ -94,6 +94,11 @@ int omni_compact_rows(const uint8_t* active, const int32_t* block_active, int n_
 size_t omni_probe_mass_workspace(int n_q_heads, int n_blocks);
 int omni_probe_mass(const double* pooled_q, const double* pooled_k, int n_q_heads, int n_kv_heads, int n_blocks,
                     int head_dim, double* mass, void* workspace, void* stream);
+/* Same result, additionally leaving the pooled scores S [Hq, nb, nb] and the
+ * row statistics (max, sum) [Hq, nb, 2] in the workspace — the materialised
+ * BlockProbeMap of block_probe.py:44-64 (validation / probe_attention API). */
+int omni_probe_mass_map(const double* pooled_q, const double* pooled_k, int n_q_heads, int n_kv_heads, int n_blocks,
+                        int head_dim, double* mass, void* workspace, void* stream);
 
 /* ---------------------------------------------------------------- K3x
  * Exact key scores (score_source = "exact"): per Q head the column mass of the

@@ -30,6 +30,7 @@ SIGNATURES = {
     "omni_compact_rows": (_c_int, [_p, _p, _c_int, _c_int, _c_int, _p, _p, _p]),
     "omni_probe_mass_workspace": (_c_size, [_c_int, _c_int]),
     "omni_probe_mass": (_c_int, [_p, _p, _c_int, _c_int, _c_int, _c_int, _p, _p, _p]),
+    "omni_probe_mass_map": (_c_int, [_p, _p, _c_int, _c_int, _c_int, _c_int, _p, _p, _p]),
     "omni_exact_mass_workspace": (_c_size, [_c_int, _c_int]),
     "omni_exact_mass": (_c_int, [_p, _p, _c_int, _c_int, _c_int, _c_int, _c_int, _p, _p, _p]),
     "omni_select": (_c_int, [_p, _c_int, _c_int, _c_int, _c_int, _c_double, _c_int, _c_int, _c_int,

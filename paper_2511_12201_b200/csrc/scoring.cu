@@ -71,14 +71,24 @@ __global__ void __launch_bounds__(256) kv_probe_kernel(const T* __restrict__ K, 
   const int r0 = J * block, r1 = min(N, r0 + block);
   double all[8] = {0, 0, 0, 0, 0, 0, 0, 0}, vis[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   const T* base = K + (size_t)g * N * d + tc * 8;
-  for (int r = r0 + tr; r < r1; r += lanes) {
-    double x[8];
-    Vec8<T>::load(base + (size_t)r * d, x);
-    const bool v = r < n_vision;
+  // four rows per lane in flight per pass (raw loads first, then the f64 sums)
+  for (int rb = r0 + tr; rb < r1; rb += 4 * lanes) {
+    Raw8<T> x[4];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      all[i] += x[i];
-      if (v) vis[i] += x[i];
+    for (int u = 0; u < 4; ++u) {
+      const int r = rb + u * lanes;
+      if (r < r1) x[u].load(base + (size_t)r * d); else x[u].zero();
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int r = rb + u * lanes;
+      const bool v = r < n_vision;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const double xi = x[u].at(i);
+        all[i] += xi;
+        if (v) vis[i] += xi;
+      }
     }
   }
   double* s_all = sh;
@@ -239,6 +249,158 @@ __global__ void __launch_bounds__(256) q_score_kernel(const T* __restrict__ Q, i
   }
 }
 
+// K2 bulk variant (bf16, d = 128, 64 <= block <= 256 rows: the hot path).
+// The CTA's whole probe block of Q (block x 256 B, up to 64 KB) is brought into
+// shared memory by four cp.async.bulk copies on mbarriers issued by one
+// thread; three CTAs per SM keep up to ~192 KB of reads in flight. Rows are
+// consumed from shared memory (16 lanes per row, 16 B each) with the float64
+// dot products, two-way softmax and lazy-row zeroing of q_score_kernel.
+// Measured at 64K (28 heads): 223 us vs 332 us for q_score_kernel; a
+// persistent double-buffered variant (one CTA of 16 warps per SM) measured
+// 343 us — the float64 instruction stream, not HBM, is the limit.
+constexpr int QSB_MAX_ROWS = 256;
+constexpr int QSB_CHUNKS = 4;
+
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
+
+__global__ void __launch_bounds__(256, 3) q_score_bulk_kernel(const __nv_bfloat16* __restrict__ Q, int N, int rep,
+                                                               int n_vision, double tau, int preserve, int block,
+                                                               const double* __restrict__ k_lazy,
+                                                               const double* __restrict__ k_act,
+                                                               uint8_t* __restrict__ active, double* __restrict__ p_act,
+                                                               double* __restrict__ pooled_q,
+                                                               int32_t* __restrict__ block_active,
+                                                               __nv_bfloat16* __restrict__ o_zero) {
+  constexpr int d = 128;
+  extern __shared__ __align__(16) uint8_t qsm[];  // [rows][256 B]
+  __shared__ __align__(8) uint64_t bars[QSB_CHUNKS];
+  __shared__ double s_pool[8][d];
+  __shared__ int s_cnt[8];
+  const int J = blockIdx.x, h = blockIdx.y, nb = gridDim.x;
+  const int g = h / rep;
+  const int r0 = J * block, nr = min(N, r0 + block) - r0;
+  const int rpc = (nr + QSB_CHUNKS - 1) / QSB_CHUNKS;  // rows per chunk
+  const uint32_t sq = smem_u32(qsm);
+  if (threadIdx.x == 0) {
+    for (int c = 0; c < QSB_CHUNKS; ++c) mbar_init(smem_u32(&bars[c]), 1);
+    fence_mbar_init();
+    const uint8_t* src = reinterpret_cast<const uint8_t*>(Q + ((size_t)h * N + r0) * d);
+    for (int c = 0; c < QSB_CHUNKS; ++c) {
+      const int lo = c * rpc, hi = min(nr, lo + rpc);
+      if (hi <= lo) continue;
+      const uint32_t bytes = (uint32_t)(hi - lo) * (d * 2);
+      mbar_expect_tx(smem_u32(&bars[c]), bytes);
+      bulk_g2s(sq + lo * (d * 2), src + (size_t)lo * (d * 2), bytes, smem_u32(&bars[c]));
+    }
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int sub = lane >> 4, cl = lane & 15;
+  double kl[8], ka[8], pool[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    kl[i] = k_lazy[(size_t)g * d + cl * 8 + i];
+    ka[i] = k_act[(size_t)g * d + cl * 8 + i];
+    pool[i] = 0.0;
+  }
+  const double scale = 1.0 / sqrt(static_cast<double>(d));
+  __syncthreads();  // barrier initialisation visible before anyone waits
+  // Each half-warp takes QSB_U consecutive rows per step (independent f64
+  // chains), then a reduce-scatter over its 16 lanes (xor 8, 4, then a
+  // butterfly over xor 2, 1): 5 shuffles per 4 rows and value instead of 16,
+  // and four lanes finalise the four rows in parallel.
+  constexpr int QSB_U = 4;
+  const int b3 = (cl >> 3) & 1, b2 = (cl >> 2) & 1;
+  const int my_u = b3 * 2 + b2;  // row of this lane after the reduce-scatter
+  int cnt = 0, waited = -1;
+  for (int base = warp * 2 * QSB_U; base < nr; base += 8 * 2 * QSB_U) {
+    const int rb = base + sub * QSB_U;  // this half-warp's first row
+    const int last = min(nr, base + 2 * QSB_U) - 1;
+    const int c = last / rpc;
+    for (int cc = waited + 1; cc <= c; ++cc) mbar_wait(smem_u32(&bars[cc]), 0);
+    waited = max(waited, c);
+    double dl[QSB_U], da[QSB_U];
+#pragma unroll
+    for (int u = 0; u < QSB_U; ++u) {
+      dl[u] = 0.0;
+      da[u] = 0.0;
+      if (rb + u < nr) {
+        const uint4 q = *reinterpret_cast<const uint4*>(qsm + (size_t)(rb + u) * (d * 2) + cl * 16);
+        const __nv_bfloat16* hv = reinterpret_cast<const __nv_bfloat16*>(&q);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const double v = static_cast<double>(__bfloat162float(hv[i]));
+          pool[i] += v;
+          dl[u] = fma(v, kl[i], dl[u]);
+          da[u] = fma(v, ka[i], da[u]);
+        }
+      }
+    }
+    auto rs_step = [&](double* v, int n, int bit, int mask) {
+#pragma unroll
+      for (int k = 0; k < n; ++k) {
+        const double lo = v[k], hi = v[k + n];
+        const double send = bit ? lo : hi, keep = bit ? hi : lo;
+        v[k] = keep + __shfl_xor_sync(0xffffffffu, send, mask);
+      }
+    };
+    rs_step(dl, 2, b3, 8); rs_step(da, 2, b3, 8);
+    rs_step(dl, 1, b2, 4); rs_step(da, 1, b2, 4);
+    double sl = dl[0] + __shfl_xor_sync(0xffffffffu, dl[0], 2);
+    double sa = da[0] + __shfl_xor_sync(0xffffffffu, da[0], 2);
+    sl += __shfl_xor_sync(0xffffffffu, sl, 1);
+    sa += __shfl_xor_sync(0xffffffffu, sa, 1);
+    const int rr = rb + my_u, r = r0 + rr;
+    int act = 1;
+    const bool fin = (cl & 3) == 0 && rr < nr;
+    if (fin) {
+      if (r < n_vision) {
+        const double l0 = sl * scale, l1 = sa * scale;
+        // max-subtracted two-way softmax (query_select.py:63-68)
+        const double p = (l1 >= l0) ? 1.0 / (exp(l0 - l1) + 1.0) : (exp(l1 - l0) / (1.0 + exp(l1 - l0)));
+        act = (p > tau) ? 1 : 0;
+        if (p_act) p_act[(size_t)h * n_vision + r] = p;
+      }
+      if (preserve && h == 0) act = 1;
+      active[(size_t)h * N + r] = static_cast<uint8_t>(act);
+      cnt += act;
+    }
+    // lazy rows of this half-warp -> zero output rows (16 B per lane per row)
+    const unsigned lazy = __ballot_sync(0xffffffffu, fin && !act);
+    if (o_zero) {
+#pragma unroll
+      for (int u = 0; u < QSB_U; ++u) {
+        const int src_lane = sub * 16 + ((u >> 1) & 1) * 8 + (u & 1) * 4;
+        if ((lazy >> src_lane) & 1u)
+          *reinterpret_cast<uint4*>(o_zero + ((size_t)h * N + r0 + rb + u) * d + cl * 8) = make_uint4(0, 0, 0, 0);
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) pool[i] += __shfl_xor_sync(0xffffffffu, pool[i], 16);
+  if (sub == 0) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s_pool[warp][cl * 8 + i] = pool[i];
+  }
+  cnt = warp_sum(cnt);
+  if (lane == 0) s_cnt[warp] = cnt;
+  __syncthreads();
+  if (threadIdx.x < d) {
+    double t = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) t += s_pool[w][threadIdx.x];
+    pooled_q[((size_t)h * nb + J) * d + threadIdx.x] = t / static_cast<double>(nr);
+  }
+  if (threadIdx.x == 0) {
+    int t = 0;
+    for (int w = 0; w < 8; ++w) t += s_cnt[w];
+    block_active[(size_t)h * nb + J] = t;
+  }
+}
+
 // ------------------------------------------------------------- compaction
 // CTA (block J, head h): offset = active rows in earlier blocks, then a
 // block-wide exclusive scan of this block's flags.
@@ -281,26 +443,45 @@ __global__ void __launch_bounds__(256) compact_rows_kernel(const uint8_t* __rest
 }
 
 // ------------------------------------------------------------------ gather
-// One warp per destination row: 16-byte lane copies of a bf16/f32 row.
+// dst[g, r] = src[g, idx[g, r]]: each warp moves GR_ROWS rows per pass with
+// 16-byte lane copies (256-byte bf16 rows: two rows per warp instruction),
+// all loads of a pass issued before the stores so several KB are in flight
+// per warp; rows [count, roundup(count, pad)) are zero-filled.
+constexpr int GR_ROWS = 8;
+
 __global__ void __launch_bounds__(256) gather_rows_kernel(const uint8_t* __restrict__ src, int src_rows,
                                                           int row_bytes, const int32_t* __restrict__ idx,
                                                           int idx_stride, const int32_t* __restrict__ counts,
                                                           int count_const, uint8_t* __restrict__ dst, int dst_rows,
                                                           int pad_rows) {
   const int g = blockIdx.y;
-  const int r = blockIdx.x * 8 + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int cnt = counts ? counts[g] : count_const;
   const int lim = min(dst_rows, ((cnt + pad_rows - 1) / pad_rows) * pad_rows);
-  if (r >= lim) return;
-  uint8_t* o = dst + ((size_t)g * dst_rows + r) * row_bytes;
-  if (r < cnt) {
-    const int s = __ldg(idx + (size_t)g * idx_stride + r);
-    const uint8_t* i = src + ((size_t)g * src_rows + s) * row_bytes;
-    for (int c = lane * 16; c < row_bytes; c += 512)
-      *reinterpret_cast<uint4*>(o + c) = __ldg(reinterpret_cast<const uint4*>(i + c));
-  } else {
-    for (int c = lane * 16; c < row_bytes; c += 512) *reinterpret_cast<uint4*>(o + c) = make_uint4(0, 0, 0, 0);
+  const int chunks = row_bytes >> 4;  // 16-byte chunks per row
+  const int r0 = (blockIdx.x * 8 + warp) * GR_ROWS;
+  if (r0 >= lim) return;
+  const int total = GR_ROWS * chunks;  // chunks this warp moves
+  for (int base = 0; base < total; base += 32 * 4) {
+    uint4 v[4];
+    int rr[4], cc[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int e = base + u * 32 + lane;
+      rr[u] = r0 + e / chunks;
+      cc[u] = e % chunks;
+      v[u] = make_uint4(0, 0, 0, 0);
+      if (e < total && rr[u] < cnt) {
+        const int sidx = __ldg(idx + (size_t)g * idx_stride + rr[u]);
+        v[u] = __ldg(reinterpret_cast<const uint4*>(src + ((size_t)g * src_rows + sidx) * row_bytes) + cc[u]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int e = base + u * 32 + lane;
+      if (e < total && rr[u] < lim)
+        reinterpret_cast<uint4*>(dst + ((size_t)g * dst_rows + rr[u]) * row_bytes)[cc[u]] = v[u];
+    }
   }
 }
 
@@ -361,7 +542,17 @@ extern "C" int omni_q_score(const void* Q, int dtype, int n_q_heads, int n_kv_he
   dim3 grid(nblocks(seq_len, block_size), n_q_heads);
   const int rep = n_q_heads / n_kv_heads;
   __nv_bfloat16* oz = static_cast<__nv_bfloat16*>(O_zero);
-  if (dtype == OMNI_DTYPE_BF16)
+  if (dtype == OMNI_DTYPE_BF16 && head_dim == 128 && block_size >= 64 && block_size <= QSB_MAX_ROWS) {
+    const int shm = block_size * head_dim * 2;
+    static int attr = 0;
+    if (shm > attr) {
+      OMNI_CUDA_TRY(cudaFuncSetAttribute(q_score_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, shm));
+      attr = shm;
+    }
+    q_score_bulk_kernel<<<grid, 256, shm, s>>>(static_cast<const __nv_bfloat16*>(Q), seq_len, rep, n_vision, tau,
+                                               preserve_first_head, block_size, k_lazy, k_act, active, p_act, pooled_q,
+                                               block_active, oz);
+  } else if (dtype == OMNI_DTYPE_BF16)
     q_score_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(Q), seq_len, head_dim, rep,
                                                        n_vision, tau, preserve_first_head, block_size, k_lazy, k_act,
                                                        active, p_act, pooled_q, block_active, oz);
@@ -390,7 +581,7 @@ extern "C" int omni_gather_rows(const void* src, int dtype, int n_groups, int sr
   const int esz = dtype == OMNI_DTYPE_BF16 ? 2 : 4;
   const int row_bytes = head_dim * esz;
   OMNI_CHECK(row_bytes % 16 == 0, OMNI_E_SHAPE, "row bytes must be a multiple of 16");
-  dim3 grid(nblocks(dst_rows, 8), n_groups);
+  dim3 grid(nblocks(dst_rows, 8 * GR_ROWS), n_groups);
   if (grid.x == 0 || n_groups == 0) return OMNI_OK;
   gather_rows_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
       static_cast<const uint8_t*>(src), src_rows, row_bytes, idx, idx_stride, counts, count_const,

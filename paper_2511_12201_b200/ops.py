@@ -111,7 +111,8 @@ def probe_mass(pooled_q: torch.Tensor, pooled_k: torch.Tensor, return_workspace:
     hkv = pooled_k.shape[0]
     mass = torch.empty(hq, nb, device=pooled_q.device, dtype=torch.float64)
     ws = torch.empty(_lib.size("omni_probe_mass_workspace", hq, nb) // 8, device=pooled_q.device, dtype=torch.float64)
-    _lib.call("omni_probe_mass", _p(pooled_q), _p(pooled_k), hq, hkv, nb, d, _p(mass), _p(ws), _stream())
+    _lib.call("omni_probe_mass_map" if return_workspace else "omni_probe_mass", _p(pooled_q), _p(pooled_k), hq, hkv,
+              nb, d, _p(mass), _p(ws), _stream())
     if return_workspace:
         return mass, ws
     return mass
