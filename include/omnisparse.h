@@ -156,6 +156,14 @@ int omni_sparse_attn_fwd(const void* Q, const void* K_sel, const void* V_sel, co
                          const int32_t* counts, const int32_t* selected, const int32_t* sel_counts, int n_q_heads,
                          int n_kv_heads, int seq_len, int head_dim, int cap, int sink_index, void* O, float* lse,
                          void* stream);
+/* Same, with a device int32 status word (caller-owned, 4 bytes): enables the
+ * deferred-agreement fast kernel, backed by the safe kernel that re-runs the
+ * launch only when the fast one flagged a logit jump beyond 2^64 (status is
+ * left 1 in that case). status == NULL is omni_sparse_attn_fwd. */
+int omni_sparse_attn_fwd_ex(const void* Q, const void* K_sel, const void* V_sel, const void* V, const int32_t* rows,
+                            const int32_t* counts, const int32_t* selected, const int32_t* sel_counts, int n_q_heads,
+                            int n_kv_heads, int seq_len, int head_dim, int cap, int sink_index, void* O, float* lse,
+                            int32_t* status, void* stream);
 
 /* ---------------------------------------------------------------- K5
  * Backward of K4 (no reference counterpart: the reference has no autograd).

@@ -39,6 +39,8 @@ SIGNATURES = {
                                   _c_int, _p]),
     "omni_sparse_attn_fwd": (_c_int, [_p, _p, _p, _p, _p, _p, _p, _p, _c_int, _c_int, _c_int, _c_int, _c_int,
                                       _c_int, _p, _p, _p]),
+    "omni_sparse_attn_fwd_ex": (_c_int, [_p, _p, _p, _p, _p, _p, _p, _p, _c_int, _c_int, _c_int, _c_int, _c_int,
+                                         _c_int, _p, _p, _p, _p]),
     "omni_sparse_attn_bwd_workspace": (_c_size, [_c_int, _c_int]),
     "omni_sparse_attn_bwd": (_c_int, [_p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _c_int, _c_int, _c_int, _c_int,
                                       _c_int, _p, _p, _p, _p, _p, _p]),

@@ -87,14 +87,18 @@ __device__ __forceinline__ constexpr bool use_poly(int pair) {
 // lane 0 of every softmax / MMA warp, read back with omni_debug_fwd_trace.
 __device__ unsigned long long g_fwd_trace[8];
 
-template <int POLY, bool TRACE = false>
+// FAST: deferred agreement between the two halves of a row (see the tile loop);
+// a tile whose logits jump by more than 2^64 over the running max sets
+// *status and the launch is redone by the FAST = false kernel (only_if).
+template <int POLY, bool TRACE = false, bool FAST = false>
 __global__ void __launch_bounds__(NTHREADS, 1)
 sparse_fwd_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
                   const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __restrict__ Vorig,
                   const int32_t* __restrict__ rows, const int32_t* __restrict__ counts,
                   const int32_t* __restrict__ sel, const int32_t* __restrict__ sel_counts, int Hq, int rep, int N,
                   int cap, int sel_stride, int sink, int n_tiles_max, __nv_bfloat16* __restrict__ O,
-                  float* __restrict__ lse) {
+                  float* __restrict__ lse, int* __restrict__ status, const int* __restrict__ only_if) {
+  if (only_if != nullptr && *(volatile const int*)only_if == 0) return;  // fallback launch not needed
   extern __shared__ uint8_t smem_raw[];
   const int L = blockIdx.x;
   const int h = L % Hq;
@@ -257,6 +261,7 @@ sparse_fwd_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constan
     const int nt = x ? ntB : ntA;
     const uint32_t tl = tmem + ((uint32_t)(quarter * 32) << 16);
     float m_run = -INFINITY, l_run = 0.f;
+    float pend_alpha = 1.f;  // FAST: O rescale agreed after the previous tile's release
     if (nt > 0) {
       // Q half-row -> swizzled K-major smem tile (A operand of S = Q K^T).
       uint8_t* q_gen = smem + OFF_Q + x * TILE + hf * ATOM;
@@ -349,6 +354,77 @@ sparse_fwd_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constan
           tmem_st16(tl + col_s(x) + cb + q * 16, pk);  // P over this thread's own, already-read S columns
           return rs;
         };
+        // FAST path chunk: exponentials against the shared running max only.
+        auto chunk_fast = [&](int q, float m_cur, float& cmax) -> float {
+          uint32_t sr[32], pk[16];
+          __syncwarp();
+          tmem_ld32(tl + col_s(x) + cb + q * 32, sr);
+          tmem_wait_ld();
+          if (!full) {
+#pragma unroll
+            for (int c = 0; c < 32; ++c)
+              if (q * 32 + c >= lim) sr[c] = __float_as_uint(-INFINITY);
+          }
+          float m0 = -INFINITY, m1 = -INFINITY;
+#pragma unroll
+          for (int c = 0; c < 32; c += 4) {
+            m0 = fmax3(m0, __uint_as_float(sr[c]), __uint_as_float(sr[c + 1]));
+            m1 = fmax3(m1, __uint_as_float(sr[c + 2]), __uint_as_float(sr[c + 3]));
+          }
+          const float rs = full ? exps(std::true_type{}, sr, -m_cur, pk) : exps(std::false_type{}, sr, -m_cur, pk);
+          cmax = fmaxf(cmax, fmaxf(m0, m1) * sl2);
+          tmem_st16(tl + col_s(x) + cb + q * 16, pk);
+          return rs;
+        };
+        if constexpr (FAST) {
+          // Deferred agreement: unless some row of the warp sees its first
+          // visible keys (both halves evaluate this identically), exponentiate
+          // against the shared running max, release P at once, and settle any
+          // growth beyond 2^8 afterwards, off the S -> P -> MMA critical path:
+          // the OR-barrier and max exchange then run while the tensor core
+          // works, and O is rescaled at the next tile (or in the epilogue).
+          // A jump beyond 2^64 (P could overflow) flags the launch for a redo.
+          {
+            if (__any_sync(0xffffffffu, pend_alpha != 1.f)) {  // PV_X(j-1) complete (it precedes QK_X(j))
+#pragma unroll
+              for (int q = 0; q < 2; ++q) {
+                uint32_t o[32];
+                __syncwarp();
+                tmem_ld32(tl + col_o(x) + cb + q * 32, o);
+                tmem_wait_ld();
+#pragma unroll
+                for (int c = 0; c < 32; ++c) o[c] = __float_as_uint(__uint_as_float(o[c]) * pend_alpha);
+                tmem_st32(tl + col_o(x) + cb + q * 32, o);
+              }
+              pend_alpha = 1.f;
+            }
+          }
+          if (!__any_sync(0xffffffffu, m_run == -INFINITY && lim_row > 0)) {
+            float cmax = -INFINITY, mu0, mu1;
+            float m_cur = m_run;
+            const float rs = chunk_fast(0, m_cur, cmax) + chunk_fast(1, m_cur, cmax);
+            (void)mu0; (void)mu1;
+            tmem_wait_st();
+            tc_fence_before();
+            mbar_arrive(B(B_PF + x));
+            if (cmax > m_run + 64.0f) atomicExch(status, 1);
+            const float tgt = cmax > m_run + 8.0f ? ceilf(cmax) : m_run;
+            if (named_bar_red_or(bid, 2 * 32, tgt != m_run)) {
+              s_xch[x][i][hf] = tgt;
+              named_bar_sync(bid, 2 * 32);
+              const float m_fin = fmaxf(tgt, s_xch[x][i][hf ^ 1]);
+              named_bar_sync(bid, 2 * 32);
+              const float alpha = pow2_int(m_run - m_fin);
+              l_run = (l_run + rs) * alpha;
+              pend_alpha = alpha;
+              m_run = m_fin;
+            } else {
+              l_run += rs;
+            }
+            tick(3);
+            continue;
+          }
+        }
         float m_cur = m_run, cmax = -INFINITY, mu0, mu1;
         const float rs0 = chunk(0, m_cur, cmax, mu0);
         tick(1);
@@ -420,7 +496,8 @@ sparse_fwd_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constan
     // ------------------------------------------------------ epilogue
     uint4* dst = reinterpret_cast<uint4*>(O + ((size_t)h * N + pos) * D + cb);
     if (nt > 0) {
-      const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
+      // (a rescale agreed after the last tile applies to O, already to l)
+      const float inv = l_run > 0.f ? pend_alpha / l_run : 0.f;
 #pragma unroll
       for (int q = 0; q < 2; ++q) {
         uint32_t o[32];
@@ -472,20 +549,24 @@ int omni_sparse_attn_fwd_pair(const void* Q, const void* K_sel, const void* V_se
                               int n_q_heads, int n_kv_heads, int seq_len, int cap, int sink_index, void* O,
                               float* lse, int poly, cudaStream_t stream);
 
-extern "C" int omni_sparse_attn_fwd(const void* Q, const void* K_sel, const void* V_sel, const void* V,
-                                    const int32_t* rows, const int32_t* counts, const int32_t* selected,
-                                    const int32_t* sel_counts, int n_q_heads, int n_kv_heads, int seq_len,
-                                    int head_dim, int cap, int sink_index, void* O, float* lse, void* stream) {
+// status: device int workspace (nullable). With it the FAST kernel runs first
+// and the safe kernel is launched behind it, exiting at once unless a tile's
+// logits jumped beyond 2^64 over the running max (then it redoes everything).
+extern "C" int omni_sparse_attn_fwd_ex(const void* Q, const void* K_sel, const void* V_sel, const void* V,
+                                       const int32_t* rows, const int32_t* counts, const int32_t* selected,
+                                       const int32_t* sel_counts, int n_q_heads, int n_kv_heads, int seq_len,
+                                       int head_dim, int cap, int sink_index, void* O, float* lse, int32_t* status,
+                                       void* stream) {
   OMNI_CHECK(head_dim == 128, OMNI_E_SHAPE, "sparse attention kernel requires head_dim == 128");
   OMNI_CHECK(n_kv_heads >= 1 && n_q_heads % n_kv_heads == 0, OMNI_E_SHAPE, "n_q_heads must be a multiple of n_kv_heads");
   OMNI_CHECK(cap >= 128 && cap % 128 == 0, OMNI_E_SHAPE, "cap must be a positive multiple of 128");
   OMNI_CHECK(sink_index >= 0 && sink_index < seq_len, OMNI_E_LAYOUT, "sink_index outside the sequence");
   OMNI_CHECK(seq_len >= 1, OMNI_E_SHAPE, "empty sequence");
   // Kernel choice: the single-CTA two-Q-tile ping-pong kernel below by
-  // default (measured fastest: 10.0 ms vs 11.0 ms at the 64K bench workload);
-  // OMNI_FWD_IMPL=pair selects the CTA-pair kernel of attn_fwd2.cu (faster
-  // MMA/TMA pipeline, 6.8 vs 7.2 ms without softmax work, but its one-tile-per-SM
-  // softmax is the bottleneck; profiles/r01_k4_notes.md).
+  // default (measured fastest at the 64K bench workload); OMNI_FWD_IMPL=pair
+  // selects the CTA-pair kernel of attn_fwd2.cu (faster MMA/TMA pipeline, 6.8
+  // vs 7.2 ms without softmax work, but its one-tile-per-SM softmax is the
+  // bottleneck; profiles/r01_k4_notes.md).
   static const bool single = [] {
     const char* e = getenv("OMNI_FWD_IMPL");
     return !(e && strcmp(e, "pair") == 0);
@@ -494,17 +575,18 @@ extern "C" int omni_sparse_attn_fwd(const void* Q, const void* K_sel, const void
     const char* e = getenv("OMNI_FWD_POLY");
     return e ? atoi(e) : kDefaultPoly;
   }();
+  cudaStream_t st_ = static_cast<cudaStream_t>(stream);
   if (!single)
     return omni_sparse_attn_fwd_pair(Q, K_sel, V_sel, V, rows, counts, selected, sel_counts, n_q_heads, n_kv_heads,
-                                     seq_len, cap, sink_index, O, lse, poly_env, static_cast<cudaStream_t>(stream));
+                                     seq_len, cap, sink_index, O, lse, poly_env, st_);
   CUtensorMap tk, tv;
   int st = omni_make_tmap_rows(&tk, K_sel, (uint64_t)n_kv_heads * cap, 128, 2, 64, fwd::BN);
   if (st) return st;
   st = omni_make_tmap_rows(&tv, V_sel, (uint64_t)n_kv_heads * cap, 128, 2, 64, fwd::BN);
   if (st) return st;
-  // Tuning knob for the exp2 MUFU / FMA split: OMNI_FWD_POLY = number of the
-  // 16 exponential pairs per 32-column chunk on the FMA-pipe polynomial
-  // (0, 4, 6 or 8; full tiles only).
+  // Tuning knobs: OMNI_FWD_POLY = number of the 16 exponential pairs per
+  // 32-column chunk on the FMA-pipe polynomial (0, 4, 6 or 8; full tiles
+  // only); OMNI_FWD_FAST=0 disables the deferred-agreement kernel.
   static const int poly = [] {
     const char* e = getenv("OMNI_FWD_POLY");
     const int v = e ? atoi(e) : kDefaultPoly;
@@ -514,24 +596,58 @@ extern "C" int omni_sparse_attn_fwd(const void* Q, const void* K_sel, const void
     const char* e = getenv("OMNI_FWD_TRACE");
     return e && atoi(e) != 0;
   }();
-  auto kern = trace ? fwd::sparse_fwd_kernel<4, true>  // profiling: per-phase cycle accounting
+  static const bool fast_env = [] {
+    const char* e = getenv("OMNI_FWD_FAST");
+    return !(e && atoi(e) == 0);
+  }();
+  auto safe = trace ? fwd::sparse_fwd_kernel<4, true>  // profiling: per-phase cycle accounting
             : poly == -1 ? fwd::sparse_fwd_kernel<-1>  // profiling: MMA pipeline only, no softmax
             : poly == 0 ? fwd::sparse_fwd_kernel<0>
             : poly == 4 ? fwd::sparse_fwd_kernel<4>
             : poly == 8 ? fwd::sparse_fwd_kernel<8>
                         : fwd::sparse_fwd_kernel<6>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    OMNI_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fwd::SMEM_BYTES));
-    attr_set = true;
+  auto fast = poly == 0 ? fwd::sparse_fwd_kernel<0, false, true>
+            : poly == 8 ? fwd::sparse_fwd_kernel<8, false, true>
+            : poly == 6 ? fwd::sparse_fwd_kernel<6, false, true>
+                        : fwd::sparse_fwd_kernel<4, false, true>;
+  const bool use_fast = status != nullptr && fast_env && !trace && poly >= 0;
+  static bool attr_set[2] = {false, false};
+  if (!attr_set[0]) {
+    OMNI_CUDA_TRY(cudaFuncSetAttribute(safe, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fwd::SMEM_BYTES));
+    attr_set[0] = true;
+  }
+  if (use_fast && !attr_set[1]) {
+    OMNI_CUDA_TRY(cudaFuncSetAttribute(fast, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fwd::SMEM_BYTES));
+    attr_set[1] = true;
   }
   const int n_tiles = (seq_len + 2 * fwd::BM - 1) / (2 * fwd::BM);
   dim3 grid(n_tiles * n_q_heads);
-  kern<<<grid, fwd::NTHREADS, fwd::SMEM_BYTES, static_cast<cudaStream_t>(stream)>>>(
-      tk, tv, static_cast<const __nv_bfloat16*>(Q), static_cast<const __nv_bfloat16*>(V), rows, counts, selected,
-      sel_counts, n_q_heads, n_q_heads / n_kv_heads, seq_len, cap, seq_len, sink_index, n_tiles,
-      static_cast<__nv_bfloat16*>(O), lse);
+  const int rep = n_q_heads / n_kv_heads;
+  auto qp = static_cast<const __nv_bfloat16*>(Q);
+  auto vp = static_cast<const __nv_bfloat16*>(V);
+  auto op = static_cast<__nv_bfloat16*>(O);
+  if (use_fast) {
+    OMNI_CUDA_TRY(cudaMemsetAsync(status, 0, sizeof(int32_t), st_));
+    fast<<<grid, fwd::NTHREADS, fwd::SMEM_BYTES, st_>>>(tk, tv, qp, vp, rows, counts, selected, sel_counts, n_q_heads,
+                                                        rep, seq_len, cap, seq_len, sink_index, n_tiles, op, lse,
+                                                        status, nullptr);
+    safe<<<grid, fwd::NTHREADS, fwd::SMEM_BYTES, st_>>>(tk, tv, qp, vp, rows, counts, selected, sel_counts, n_q_heads,
+                                                        rep, seq_len, cap, seq_len, sink_index, n_tiles, op, lse,
+                                                        nullptr, status);
+  } else {
+    safe<<<grid, fwd::NTHREADS, fwd::SMEM_BYTES, st_>>>(tk, tv, qp, vp, rows, counts, selected, sel_counts, n_q_heads,
+                                                        rep, seq_len, cap, seq_len, sink_index, n_tiles, op, lse,
+                                                        nullptr, nullptr);
+  }
   return omni_launch_check();
+}
+
+extern "C" int omni_sparse_attn_fwd(const void* Q, const void* K_sel, const void* V_sel, const void* V,
+                                    const int32_t* rows, const int32_t* counts, const int32_t* selected,
+                                    const int32_t* sel_counts, int n_q_heads, int n_kv_heads, int seq_len,
+                                    int head_dim, int cap, int sink_index, void* O, float* lse, void* stream) {
+  return omni_sparse_attn_fwd_ex(Q, K_sel, V_sel, V, rows, counts, selected, sel_counts, n_q_heads, n_kv_heads,
+                                 seq_len, head_dim, cap, sink_index, O, lse, nullptr, stream);
 }
 
 // Profiling support (OMNI_FWD_TRACE=1): copies the 8 per-phase cycle sums

@@ -188,9 +188,21 @@ def sparse_attn_fwd(Q, K_sel, V_sel, V, rows, counts, selected, sel_counts, sink
         raise ShapeError("sparse attention consumes bf16 Q/K/V")
     if selected.shape[-1] != n:
         raise ShapeError("selected must be [Hkv, N]")
-    _lib.call("omni_sparse_attn_fwd", _p(Q), _p(K_sel), _p(V_sel), _p(V), _p(rows), _p(counts), _p(selected),
-              _p(sel_counts), hq, hkv, n, d, cap, sink_index, _p(O), _p(lse), _stream())
+    _lib.call("omni_sparse_attn_fwd_ex", _p(Q), _p(K_sel), _p(V_sel), _p(V), _p(rows), _p(counts), _p(selected),
+              _p(sel_counts), hq, hkv, n, d, cap, sink_index, _p(O), _p(lse), _p(_status_word(Q.device)), _stream())
     return O, lse
+
+
+_STATUS: dict = {}
+
+
+def _status_word(device) -> torch.Tensor:
+    """Per-device int32 status word of the fast forward kernel (caller-owned
+    workspace of omni_sparse_attn_fwd_ex; allocated once per device)."""
+    key = str(device)
+    if key not in _STATUS:
+        _STATUS[key] = torch.zeros(1, device=device, dtype=torch.int32)
+    return _STATUS[key]
 
 
 def sparse_attn_bwd(Q, K_sel, V_sel, O, dO, lse, rows, counts, selected, sel_counts):
