@@ -199,6 +199,9 @@ _STATUS: dict = {}
 def _status_word(device) -> torch.Tensor:
     """Per-device int32 status word of the fast forward kernel (caller-owned
     workspace of omni_sparse_attn_fwd_ex; allocated once per device)."""
+    device = torch.device(device)
+    if device.index is None:
+        device = torch.device(device.type, torch.cuda.current_device())
     key = str(device)
     if key not in _STATUS:
         _STATUS[key] = torch.zeros(1, device=device, dtype=torch.int32)

@@ -44,11 +44,13 @@ print(json.dumps({"scaled_err": err, "nan": bool(np.isnan(out).any()), "fallback
 
 
 JUMP = r"""
-# one late key with a huge norm: logits of later rows jump far beyond the
-# running max (> 2^64 in exp2 units) -> the fast kernel must hand over to the
-# safe re-run, and the result must still match the oracle
-import numpy as _np
-K[:, 1500, :] *= 400.0
+# one late key aligned with its group's queries and with a huge norm: the
+# logits of every later row jump far beyond the running max (> 2^64 in exp2
+# units) -> the fast kernel must hand over to the safe re-run, and the result
+# must still match the oracle
+for _g in range(K.shape[0]):
+    _u = Q[4 * _g:4 * _g + 4].mean(axis=(0, 1))
+    K[_g, 1500, :] = 2000.0 * _u / np.linalg.norm(_u)
 """
 
 
