@@ -482,12 +482,39 @@ def run_ours(args):
                                     ops.gather_rows(V, sel.selected, sel.counts, cap, 128, out=res.V_sel)),
                            args.steps, 2)
         achieved = flops / (fa_ms / 1e3) / 1e12
+        traffic = None
+        try:  # dram bytes per K4 launch from the committed ncu capture of the same workload
+            with open(os.path.join(ROOT, "profiles", "r01_k4_traffic.json")) as f:
+                traffic = json.load(f)["dram_bytes_per_launch"]
+        except Exception:  # noqa: BLE001
+            pass
         line["roofline"] = {"bound": "tensor", "kernel": "omni sparse_fwd_kernel (K4)", "achieved": achieved,
-                            "peak": tc_peak, "unit": "TFLOP/s", "frac": achieved / tc_peak, "traffic": None,
+                            "peak": tc_peak, "unit": "TFLOP/s", "frac": achieved / tc_peak, "traffic": traffic,
+                            "traffic_note": "dram__bytes_read.sum + dram__bytes_write.sum per launch "
+                                            "(profiles/r01_k4_traffic.json); K4 is tensor-bound, its DRAM traffic "
+                                            "(Q rows, K/V tiles re-read past L2, O rows) is ~1.1 GB per 9.6 ms",
                             "peak_source": f"{peak_src} bf16 burst (MEASURED_PEAKS.json)",
                             "algorithmic_flops_per_launch": flops, "launch_ms": fa_ms}
         line["breakdown_ms"] = {"select_path_K1_K2_compact_K3": sel_ms, "gather_K6": gat_ms, "sparse_fa_K4": fa_ms,
                                 "k4_share_of_step": fa_ms / ms}
+        # ----- HBM-bound kernels against the measured copy bandwidth (algorithmic bytes)
+        try:
+            hb = {}
+            k1_ms = time_cuda(lambda: ops.kv_probe(K, nv, 0, 256), args.steps, 2)
+            k1_bytes = HKV * n * D * 2
+            kl_, ka_, _ = ops.kv_probe(K, nv, 0, 256)
+            k2_ms = time_cuda(lambda: ops.q_score(Q, kl_, ka_, nv, args.tau, True, 256, O_zero=O), args.steps, 2)
+            lazy_rows = int((res.active == 0).sum())
+            k2_bytes = HQ * n * D * 2 + lazy_rows * D * 2 + HQ * n  # Q read, lazy O rows zeroed, flags
+            bsum = int(sel.info[4:].sum())
+            k6_bytes = 2 * (bsum * D * 2 + HKV * cap * D * 2)  # K and V: selected rows read, padded rows written
+            for name, kms, kb in (("K1_kv_probe", k1_ms, k1_bytes), ("K2_q_score", k2_ms, k2_bytes),
+                                  ("K6_gather_KV", gat_ms, k6_bytes)):
+                gbs = kb / (kms / 1e3) / 1e9
+                hb[name] = {"ms": kms, "bytes": kb, "achieved_GBs": gbs, "frac_of_peak": gbs / hbm_peak}
+            line["hbm_kernels"] = hb
+        except Exception as e:  # noqa: BLE001
+            line["hbm_kernels"] = {"error": str(e)[:200]}
         n_ours, n_all, names = count_launches(step)
         line["gpu_launches"] = n_ours * args.steps
         line["gpu_launches_per_step"] = {"ours": n_ours, "all": n_all, "kernels": names}
