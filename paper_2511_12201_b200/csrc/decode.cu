@@ -20,6 +20,8 @@
 //   decode_combine_kernel merges the per-chunk (max, sum, acc) partials.
 // HBM-bound: bytes = fetched vision + text + answer K/V rows, once each.
 #include <math.h>
+#include <stdlib.h>
+#include <string.h>
 
 #include "common.cuh"
 
@@ -278,10 +280,268 @@ __global__ void decode_combine_kernel(const float* __restrict__ part_ml, const f
   }
 }
 
+// ---------------------------------------------------------------- K7 v3
+// TMA-staged variant (default): persistent CTAs (one per SM) walk the
+// (chunk, KV group, sequence) work items; a producer warp streams 64-key K and
+// V tiles of each segment (vision / text / answer, 2-D tensor maps with
+// SWIZZLE_128B) into an NSTG-stage shared-memory ring that runs ahead across
+// work items, so each SM keeps up to NSTG x 32 KB of HBM reads in flight with
+// no register staging. Four consumer warps take 16 keys of each tile: B
+// fragments of S = Q K^T come from ldmatrix.x4 and of O += P V from
+// ldmatrix.x4.trans (conflict-free on the swizzled tiles), the MMA and softmax
+// math is that of decode_partial_kernel.
+constexpr int TK = 64, NSTG = 4, NCW = 4;
+constexpr uint32_t TATOM = TK * 128;      // 64 rows x 128 B
+constexpr uint32_t TTILE = 2 * TATOM;     // 64 keys x 128 d bf16 = 16 KB
+constexpr uint32_t TSTAGE = 2 * TTILE;    // K + V
+constexpr uint32_t TSMEM = NSTG * TSTAGE + 1024;
+
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t* r) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t* r) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr));
+}
+// byte offset of 16-byte chunk c (0..15 over d = 128) of key row r in a tile
+__device__ __forceinline__ uint32_t toff(int r, int c) {
+  return (uint32_t)(c >> 3) * TATOM + (uint32_t)r * 128u + ((uint32_t)((c & 7) ^ (r & 7)) << 4);
+}
+
+struct DecItem {
+  int s, g, c, lo, hi, vl, any;
+};
+
+__device__ __forceinline__ DecItem dec_item(int t, int nc, int Hq, int Hkv, int nt, int na,
+                                            const int32_t* __restrict__ vlen, const uint8_t* __restrict__ flags) {
+  DecItem it;
+  it.c = t % nc;
+  it.g = (t / nc) % Hkv;
+  it.s = t / (nc * Hkv);
+  const int rep = Hq / Hkv;
+  int any = 0;
+  for (int r = 0; r < rep; ++r) any |= flags[(size_t)it.s * Hq + it.g * rep + r];
+  it.any = any;
+  it.vl = vlen[it.s];
+  const int k_start = any ? 0 : it.vl;  // skip the vision segment when every head is lazy
+  const int k_end = it.vl + nt + na;
+  it.lo = k_start + it.c * CTA_KEYS;
+  it.hi = min(k_end, it.lo + CTA_KEYS);
+  return it;
+}
+
+// tile starting at key k of item `it`: segment, local row, valid keys
+__device__ __forceinline__ void dec_tile(const DecItem& it, int k, int nt, int& seg, int& row, int& nvalid) {
+  int seg_lo, seg_hi;
+  if (k < it.vl) { seg = 0; seg_lo = 0; seg_hi = it.vl; }
+  else if (k < it.vl + nt) { seg = 1; seg_lo = it.vl; seg_hi = it.vl + nt; }
+  else { seg = 2; seg_lo = it.vl + nt; seg_hi = it.hi; }
+  row = k - seg_lo;
+  nvalid = min(TK, min(seg_hi, it.hi) - k);
+}
+
+__global__ void __launch_bounds__((NCW + 1) * 32, 1) decode_partial_tma_kernel(
+    const __grid_constant__ CUtensorMap tm_vk, const __grid_constant__ CUtensorMap tm_vv,
+    const __grid_constant__ CUtensorMap tm_tk, const __grid_constant__ CUtensorMap tm_tv,
+    const __grid_constant__ CUtensorMap tm_ak, const __grid_constant__ CUtensorMap tm_av,
+    const __nv_bfloat16* __restrict__ q, const int32_t* __restrict__ vlen, int nt, int na, int Hq, int Hkv,
+    int vcap, int acap, const uint8_t* __restrict__ flags, float* __restrict__ part_ml,
+    float* __restrict__ part_acc, int n_chunks, int total_items) {
+  extern __shared__ uint8_t dsm_raw[];
+  __shared__ __align__(8) uint64_t full_bar[NSTG], empty_bar[NSTG];
+  __shared__ float s_ml[NCW][MAXREP][2];
+  __shared__ float s_acc[NCW][MAXREP][D];
+  uint8_t* dsm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dsm_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sbase = smem_u32(dsm);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < NSTG; ++i) {
+      mbar_init(smem_u32(&full_bar[i]), 1);
+      mbar_init(smem_u32(&empty_bar[i]), NCW);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const int rep = Hq / Hkv;
+
+  if (warp == NCW) {
+    // ------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      tma_prefetch_desc(&tm_vk); tma_prefetch_desc(&tm_vv);
+      tma_prefetch_desc(&tm_tk); tma_prefetch_desc(&tm_tv);
+      tma_prefetch_desc(&tm_ak); tma_prefetch_desc(&tm_av);
+      uint32_t n = 0;
+      for (int t = blockIdx.x; t < total_items; t += gridDim.x) {
+        const DecItem it = dec_item(t, n_chunks, Hq, Hkv, nt, na, vlen, flags);
+        const int sg = it.s * Hkv + it.g;
+        for (int k = it.lo; k < it.hi; k += TK) {
+          int seg, row, nv;
+          dec_tile(it, k, nt, seg, row, nv);
+          k += nv - TK;  // next tile starts after this tile's valid keys (segment-aligned)
+          const int st = n % NSTG;
+          if (n >= NSTG) mbar_wait(smem_u32(&empty_bar[st]), ((n / NSTG) - 1) & 1);
+          const uint32_t fb = smem_u32(&full_bar[st]);
+          mbar_expect_tx(fb, TSTAGE);
+          const CUtensorMap* mk = seg == 0 ? &tm_vk : seg == 1 ? &tm_tk : &tm_ak;
+          const CUtensorMap* mv = seg == 0 ? &tm_vv : seg == 1 ? &tm_tv : &tm_av;
+          const int base = seg == 0 ? sg * vcap : seg == 1 ? sg * nt : sg * acap;
+          const uint32_t kd = sbase + st * TSTAGE, vd = kd + TTILE;
+          tma_load_2d(kd, mk, fb, 0, base + row);
+          tma_load_2d(kd + TATOM, mk, fb, 64, base + row);
+          tma_load_2d(vd, mv, fb, 0, base + row);
+          tma_load_2d(vd + TATOM, mv, fb, 64, base + row);
+          ++n;
+        }
+      }
+    }
+    return;
+  }
+  // ------------------------------------------------------ consumers
+  const int r4 = lane & 3, gid = lane >> 2;
+  const bool row_valid = gid < rep;
+  const float sl2 = static_cast<float>(kLog2e / sqrt(static_cast<double>(D)));
+  uint32_t n = 0;
+  for (int t = blockIdx.x; t < total_items; t += gridDim.x) {
+    const DecItem it = dec_item(t, n_chunks, Hq, Hkv, nt, na, vlen, flags);
+    const bool row_vis = row_valid && flags[(size_t)it.s * Hq + it.g * rep + (row_valid ? gid : 0)];
+    // Q A-fragments, natural head-dim order: k-step ks covers d = 16 ks .. +15
+    uint32_t qa[8][4];
+    {
+      const uint32_t* qw =
+          reinterpret_cast<const uint32_t*>(q + ((size_t)it.s * Hq + it.g * rep + (row_valid ? gid : 0)) * D);
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks) {
+        qa[ks][0] = row_valid ? __ldg(qw + ks * 8 + r4) : 0u;      // d 16ks + 2 r4, +1
+        qa[ks][1] = 0u;                                             // rows 8..15: padding
+        qa[ks][2] = row_valid ? __ldg(qw + ks * 8 + 4 + r4) : 0u;  // d 16ks + 8 + 2 r4, +1
+        qa[ks][3] = 0u;
+      }
+    }
+    float m_run = -INFINITY, l_run = 0.f;
+    float acc[16][4];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
+    for (int k = it.lo; k < it.hi; k += TK) {
+      int seg, row, nv;
+      dec_tile(it, k, nt, seg, row, nv);
+      const int key0 = k;
+      k += nv - TK;
+      const int st = n % NSTG;
+      mbar_wait(smem_u32(&full_bar[st]), (n / NSTG) & 1);
+      const uint32_t kt = sbase + st * TSTAGE, vt = kt + TTILE;
+      const int w0 = warp * 16;  // this warp's first key of the tile
+      if (w0 < nv) {
+        // ---- S = Q K^T over 16 keys (two n-tiles of 8)
+        float sc[2][4];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) sc[u][0] = sc[u][1] = sc[u][2] = sc[u][3] = 0.f;
+        const int mi = lane >> 3, rr = lane & 7;
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks) {
+          uint32_t b[4];
+          // matrices: (keys 0-7, d lo) (keys 0-7, d hi) (keys 8-15, d lo) (keys 8-15, d hi)
+          ldsm_x4(kt + toff(w0 + (mi >> 1) * 8 + rr, 2 * ks + (mi & 1)), b);
+          mma_bf16_16816(sc[0], qa[ks], b[0], b[1]);
+          mma_bf16_16816(sc[1], qa[ks], b[2], b[3]);
+        }
+        // ---- mask (keys beyond the tile; vision keys for lazy heads), online softmax
+        float x[4];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int kk = w0 + 8 * u + 2 * r4 + e;  // key within the tile
+            const bool ok = row_valid && kk < nv && (seg != 0 || row_vis);
+            x[2 * u + e] = ok ? sc[u][e] * sl2 : -INFINITY;
+          }
+        }
+        float mt = fmaxf(fmaxf(x[0], x[1]), fmaxf(x[2], x[3]));
+        mt = fmaxf(mt, __shfl_xor_sync(0xffffffffu, mt, 1));
+        mt = fmaxf(mt, __shfl_xor_sync(0xffffffffu, mt, 2));
+        const float m_new = fmaxf(m_run, mt);
+        if (m_new > m_run + 8.0f) {  // lazy rescale of this row's accumulator
+          const float alpha = (m_run == -INFINITY) ? 0.f : fast_exp2(m_run - m_new);
+          l_run *= alpha;
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            acc[i][0] *= alpha;
+            acc[i][1] *= alpha;
+          }
+          m_run = m_new;
+        }
+        const float mu = (m_run == -INFINITY) ? 0.f : m_run;
+        float p[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          p[e] = fast_exp2(x[e] - mu);
+          l_run += p[e];
+        }
+        uint32_t pa[4] = {pack_bf16x2(p[0], p[1]), 0u, pack_bf16x2(p[2], p[3]), 0u};
+        // ---- O += P V over 16 d n-tiles (pairs from one ldmatrix.x4.trans)
+#pragma unroll
+        for (int j = 0; j < 16; j += 2) {
+          uint32_t b[4];
+          // matrices: (keys 0-7, d 8j) (keys 8-15, d 8j) (keys 0-7, d 8j+8) (keys 8-15, d 8j+8)
+          ldsm_x4_t(vt + toff(w0 + (mi & 1) * 8 + rr, j + (mi >> 1)), b);
+          mma_bf16_16816(acc[j], pa, b[0], b[1]);
+          mma_bf16_16816(acc[j + 1], pa, b[2], b[3]);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&empty_bar[st]));
+      ++n;
+    }
+    // ---- combine the consumer warps, write this item's partial per Q head
+    l_run += __shfl_xor_sync(0xffffffffu, l_run, 1);
+    l_run += __shfl_xor_sync(0xffffffffu, l_run, 2);
+    if (row_valid) {
+      if (r4 == 0) {
+        s_ml[warp][gid][0] = m_run;
+        s_ml[warp][gid][1] = l_run;
+      }
+      // C fragment of n-tile j: acc[j][0/1] = O[row gid][d = 8 j + 2 r4 + {0,1}]
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        s_acc[warp][gid][8 * j + 2 * r4] = acc[j][0];
+        s_acc[warp][gid][8 * j + 2 * r4 + 1] = acc[j][1];
+      }
+    }
+    named_bar_sync(1, NCW * 32);
+    for (int e = threadIdx.x; e < rep * D; e += NCW * 32) {
+      const int r = e / D, col = e % D;
+      float M = -INFINITY;
+#pragma unroll
+      for (int w = 0; w < NCW; ++w) M = fmaxf(M, s_ml[w][r][0]);
+      float L = 0.f, o = 0.f;
+#pragma unroll
+      for (int w = 0; w < NCW; ++w) {
+        const float m = s_ml[w][r][0];
+        if (m == -INFINITY) continue;
+        const float wt = fast_exp2(m - M);
+        L += wt * s_ml[w][r][1];
+        o += wt * s_acc[w][r][col];
+      }
+      const size_t pb = ((size_t)it.s * Hq + it.g * rep + r) * n_chunks + it.c;
+      part_acc[pb * D + col] = o;
+      if (col == 0) {
+        part_ml[pb * 2 + 0] = M;
+        part_ml[pb * 2 + 1] = L;
+      }
+    }
+    named_bar_sync(1, NCW * 32);  // partial slots free for the next item
+  }
+}
+
 }  // namespace dec
 }  // namespace omni
 
 using namespace omni;
+
+int omni_make_tmap_rows(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols_elems, int elem_bytes,
+                        uint32_t box_cols, uint32_t box_rows);
 
 static int dec_chunks(int vcap, int n_text, int n_answer) {
   return (vcap + n_text + n_answer + dec::CTA_KEYS - 1) / dec::CTA_KEYS;
@@ -313,12 +573,46 @@ extern "C" int omni_decode_step(const void* q, const void* vision_k, const void*
   dec::decode_flags_kernel<<<dim3(n_q_heads, batch), 32, 0, st>>>(static_cast<const __nv_bfloat16*>(q), k_lazy, k_act,
                                                                    n_q_heads, n_kv_heads, tau, preserve_first_head,
                                                                    flags_override, flags);
-  dec::decode_partial_kernel<<<dim3(nc, n_kv_heads, batch), 128, 0, st>>>(
-      static_cast<const __nv_bfloat16*>(q), static_cast<const __nv_bfloat16*>(vision_k),
-      static_cast<const __nv_bfloat16*>(vision_v), vision_len, static_cast<const __nv_bfloat16*>(text_k),
-      static_cast<const __nv_bfloat16*>(text_v), n_text, static_cast<const __nv_bfloat16*>(answer_k),
-      static_cast<const __nv_bfloat16*>(answer_v), n_answer, n_q_heads, n_kv_heads, vcap, acap, flags, part_ml,
-      part_acc, nc);
+  // K7 implementation: TMA-staged persistent kernel by default;
+  // OMNI_DECODE_IMPL=regs selects the register-staged kernel.
+  static const bool regs = [] {
+    const char* e = getenv("OMNI_DECODE_IMPL");
+    return e && strcmp(e, "regs") == 0;
+  }();
+  if (regs) {
+    dec::decode_partial_kernel<<<dim3(nc, n_kv_heads, batch), 128, 0, st>>>(
+        static_cast<const __nv_bfloat16*>(q), static_cast<const __nv_bfloat16*>(vision_k),
+        static_cast<const __nv_bfloat16*>(vision_v), vision_len, static_cast<const __nv_bfloat16*>(text_k),
+        static_cast<const __nv_bfloat16*>(text_v), n_text, static_cast<const __nv_bfloat16*>(answer_k),
+        static_cast<const __nv_bfloat16*>(answer_v), n_answer, n_q_heads, n_kv_heads, vcap, acap, flags, part_ml,
+        part_acc, nc);
+  } else {
+    CUtensorMap m[6];
+    const uint64_t vrows = (uint64_t)batch * n_kv_heads * vcap;
+    const void* bases[6] = {vision_k, vision_v, n_text > 0 ? text_k : vision_k, n_text > 0 ? text_v : vision_v,
+                            acap > 0 ? answer_k : vision_k, acap > 0 ? answer_v : vision_v};
+    const uint64_t rows[6] = {vrows, vrows, n_text > 0 ? (uint64_t)batch * n_kv_heads * n_text : vrows,
+                              n_text > 0 ? (uint64_t)batch * n_kv_heads * n_text : vrows,
+                              acap > 0 ? (uint64_t)batch * n_kv_heads * acap : vrows,
+                              acap > 0 ? (uint64_t)batch * n_kv_heads * acap : vrows};
+    for (int i = 0; i < 6; ++i) {
+      const int rc = omni_make_tmap_rows(&m[i], bases[i], rows[i], dec::D, 2, 64, dec::TK);
+      if (rc) return rc;
+    }
+    static bool attr = false;
+    if (!attr) {
+      OMNI_CUDA_TRY(cudaFuncSetAttribute(dec::decode_partial_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)dec::TSMEM));
+      attr = true;
+    }
+    int dev = 0, sms = 148;
+    OMNI_CUDA_TRY(cudaGetDevice(&dev));
+    OMNI_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const int items = nc * n_kv_heads * batch;
+    dec::decode_partial_tma_kernel<<<min(sms, items), (dec::NCW + 1) * 32, dec::TSMEM, st>>>(
+        m[0], m[1], m[2], m[3], m[4], m[5], static_cast<const __nv_bfloat16*>(q), vision_len, n_text, n_answer,
+        n_q_heads, n_kv_heads, vcap, acap, flags, part_ml, part_acc, nc, items);
+  }
   dec::decode_combine_kernel<<<dim3(n_q_heads, batch), dec::D, 0, st>>>(part_ml, part_acc, nc, out, degenerate);
   int st_code = omni_launch_check();
   if (st_code) return st_code;
