@@ -563,7 +563,7 @@ def run_ours(args):
 
             res = None
             torch.cuda.empty_cache()
-            streamer = PrefillStreamer(HQ, HKV, n, D, nv, cfg, depth=2)
+            streamer = PrefillStreamer(HQ, HKV, n, D, nv, cfg, depth=3)
             reqs = [(hQ, hK, hV)] * args.steps
             streamer.run(reqs[:2], [hO, hO])  # warm-up
             streamer.synchronize()

@@ -114,8 +114,10 @@ class PrefillStreamer:
 
     Request i's H2D copy runs on a copy stream while request i-1 computes and
     request i-2's output drains on a second copy stream (``depth`` device
-    buffer sets rotate). Every request still pays its own copies; only their
-    latency is hidden behind other requests' kernels."""
+    buffer sets rotate; depth 3 lets the three stages run concurrently, so the
+    period approaches the slowest stage — the H2D copy at PCIe rate). Every
+    request still pays its own copies; only their latency is hidden behind
+    other requests' kernels."""
 
     def __init__(self, hq: int, hkv: int, n: int, d: int, n_vision: int, cfg: SparsityConfig = SparsityConfig(),
                  depth: int = 3, device="cuda"):
