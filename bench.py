@@ -200,9 +200,17 @@ def dense_baselines(Q, K, V, steps, warmup, use_flashinfer=False):
             qf, kf, vf = (x.transpose(0, 1).contiguous() for x in (Q, K, V))
             fi = lambda: flashinfer.single_prefill_with_kv_cache(qf, kf, vf, causal=True)
             fi()
-            out["flashinfer_ms"] = time_cuda(fi, steps, warmup)
+            out["flashinfer_fa2_ms"] = time_cuda(fi, steps, warmup)
+            # sm100 CUTLASS FMHA (JIT-compiled on first use)
+            from flashinfer.prefill import fmha_varlen
+
+            seg = torch.tensor([0, n], dtype=torch.int32, device=Q.device)
+            fc = lambda: fmha_varlen(qf, kf, vf, seg, seg, max_qo_len=n, causal=True)
+            fc()
+            out["flashinfer_cutlass_fmha_ms"] = time_cuda(fc, steps, warmup)
+            del qf, kf, vf
         except Exception as e:  # noqa: BLE001
-            out["flashinfer_error"] = str(e)[:160]
+            out["flashinfer_error"] = str(e)[:300]
     times = {k: v for k, v in out.items() if k.endswith("_ms")}
     if times:
         best = min(times, key=times.get)
