@@ -102,7 +102,7 @@ constexpr uint32_t SMEM = OFF_TMEM + 16 + 1024;
 constexpr uint32_t COL_S = 0, COL_DP = 128, COL_DQ = 256;
 }  // namespace dq
 
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(384, 1)
 dq_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
           const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
           const int32_t* __restrict__ rows, const int32_t* __restrict__ counts, const float* __restrict__ lse2c,
@@ -140,8 +140,8 @@ dq_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
       mbar_init(B(B_VE + s), 1);
     }
     mbar_init(B(B_SF), 1);
-    mbar_init(B(B_SE), 128);
-    mbar_init(B(B_DSF), 128);
+    mbar_init(B(B_SE), 256);
+    mbar_init(B(B_DSF), 256);
     mbar_init(B(B_DSE), 1);
     fence_mbar_init();
   }
@@ -176,9 +176,13 @@ dq_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && nt > 0) {
+    // whole warp runs the schedule; elect.sync picks the issuing lane
+    if (nt > 0) {
       constexpr uint32_t id_kk = idesc_bf16_f32(128, 128, 0, 0);
       constexpr uint32_t id_mn = idesc_bf16_f32(128, 128, 0, 1);
+      const uint64_t dq0 = sdesc_sw128(sb + OFF_Q, 16, 1024), ddo0 = sdesc_sw128(sb + OFF_DO, 16, 1024);
+      const uint64_t dk0 = sdesc_sw128(sb + OFF_K, 16, 1024), dv0 = sdesc_sw128(sb + OFF_V, 16, 1024);
+      const uint64_t dds0 = sdesc_sw128(sb + OFF_DS, 16, 1024), dkmn0 = sdesc_sw128(sb + OFF_K, ATOM, 1024);
       auto issue_s = [&](int j) {
         const int s = j & 1;
         mbar_wait(B(B_KF + s), (j >> 1) & 1);
@@ -186,18 +190,16 @@ dq_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
-          const uint32_t off = (kk >> 2) * ATOM + (kk & 3) * 32;
-          umma_bf16(tmem + COL_S, sdesc_sw128(sb + OFF_Q + off, 16, 1024),
-                    sdesc_sw128(sb + OFF_K + s * TILE + off, 16, 1024), id_kk, kk > 0);
+          const uint32_t off = ((kk >> 2) * ATOM + (kk & 3) * 32) >> 4;
+          umma_bf16_ws(tmem + COL_S, dq0 + off, dk0 + ((s * TILE) >> 4) + off, id_kk, kk > 0);
         }
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
-          const uint32_t off = (kk >> 2) * ATOM + (kk & 3) * 32;
-          umma_bf16(tmem + COL_DP, sdesc_sw128(sb + OFF_DO + off, 16, 1024),
-                    sdesc_sw128(sb + OFF_V + s * TILE + off, 16, 1024), id_kk, kk > 0);
+          const uint32_t off = ((kk >> 2) * ATOM + (kk & 3) * 32) >> 4;
+          umma_bf16_ws(tmem + COL_DP, ddo0 + off, dv0 + ((s * TILE) >> 4) + off, id_kk, kk > 0);
         }
-        umma_commit(B(B_VE + s));
-        umma_commit(B(B_SF));
+        umma_commit_ws(B(B_VE + s));
+        umma_commit_ws(B(B_SF));
       };
       mbar_wait(B(B_QD), 0);
       issue_s(0);
@@ -206,18 +208,21 @@ dq_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
         if (j + 1 < nt) issue_s(j + 1);
         mbar_wait(B(B_DSF), j & 1);
         tc_fence_after();
-        const uint32_t kb = sb + OFF_K + (j & 1) * TILE;
+        const uint64_t kb = dkmn0 + (((j & 1) * TILE) >> 4);
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
-          umma_bf16(tmem + COL_DQ, sdesc_sw128(sb + OFF_DS + (kk >> 2) * ATOM + (kk & 3) * 32, 16, 1024),
-                    sdesc_sw128(kb + kk * 2048, ATOM, 1024), id_mn, (j > 0 || kk > 0) ? 1u : 0u);
+          umma_bf16_ws(tmem + COL_DQ, dds0 + (((kk >> 2) * ATOM + (kk & 3) * 32) >> 4), kb + ((kk * 2048) >> 4),
+                       id_mn, (j > 0 || kk > 0) ? 1u : 0u);
         }
-        umma_commit(B(B_KE + (j & 1)));
-        umma_commit(B(B_DSE));
+        umma_commit_ws(B(B_KE + (j & 1)));
+        umma_commit_ws(B(B_DSE));
       }
     }
   } else if (warp >= 4) {
-    const int i = threadIdx.x - 128;
+    // 8 warps: two per TMEM lane quarter, each thread 64 key columns of its row
+    const int hf = (warp - 4) >> 2;
+    const int i = (warp & 3) * 32 + lane;
+    const int cb = hf * 64;
     const bool valid = i < nrows;
     const size_t ci = crow0 + i;
     const int vis = valid ? __ldg(visc + ci) : 0;
@@ -232,23 +237,23 @@ dq_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
       if (j > 0) mbar_wait(B(B_DSE), (j - 1) & 1);  // dQ MMA of j-1 finished reading dS
       const int lim = vis - j * 128;
 #pragma unroll
-      for (int c4 = 0; c4 < 4; ++c4) {
+      for (int c4 = 0; c4 < 2; ++c4) {
         uint32_t s[32], p[32];
         __syncwarp();
-        tmem_ld32(tl + COL_S + c4 * 32, s);
-        tmem_ld32(tl + COL_DP + c4 * 32, p);
+        tmem_ld32(tl + COL_S + cb + c4 * 32, s);
+        tmem_ld32(tl + COL_DP + cb + c4 * 32, p);
         tmem_wait_ld();
         uint32_t pk[16];
 #pragma unroll
         for (int c = 0; c < 32; c += 2) {
-          const int col = c4 * 32 + c;
+          const int col = cb + c4 * 32 + c;
           const float p0 = (col < lim) ? fast_exp2(__uint_as_float(s[c]) * sl2 - l2) : 0.f;
           const float p1 = (col + 1 < lim) ? fast_exp2(__uint_as_float(s[c + 1]) * sl2 - l2) : 0.f;
           pk[c / 2] = pack_bf16x2(p0 * (__uint_as_float(p[c]) - Dv), p1 * (__uint_as_float(p[c + 1]) - Dv));
         }
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          const int chunk = c4 * 4 + q;  // 16-byte chunk index along keys (0..15)
+          const int chunk = hf * 8 + c4 * 4 + q;  // 16-byte chunk index along keys (0..15)
           *reinterpret_cast<uint4*>(ds_gen + (chunk >> 3) * ATOM + swz(i, chunk & 7)) =
               make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
         }
@@ -263,12 +268,12 @@ dq_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
       tc_fence_after();
       const float scale = static_cast<float>(1.0 / sqrt(static_cast<double>(D)));
       const int pos = valid ? __ldg(rows + (size_t)h * N + r0 + i) : 0;
-      float4* dst = reinterpret_cast<float4*>(dQ + ((size_t)h * N + pos) * D);
+      float4* dst = reinterpret_cast<float4*>(dQ + ((size_t)h * N + pos) * D + cb);
 #pragma unroll
-      for (int c4 = 0; c4 < 4; ++c4) {
+      for (int c4 = 0; c4 < 2; ++c4) {
         uint32_t o[32];
         __syncwarp();
-        tmem_ld32(tl + COL_DQ + c4 * 32, o);
+        tmem_ld32(tl + COL_DQ + cb + c4 * 32, o);
         tmem_wait_ld();
         if (valid) {
 #pragma unroll
@@ -311,7 +316,7 @@ struct DkvIter {
   int h0, rep, first_tile[16], n_tiles[16], total;
 };
 
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(384, 1)
 dkv_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
            const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
            const int32_t* __restrict__ rows, const int32_t* __restrict__ counts, const int32_t* __restrict__ sel,
@@ -369,11 +374,11 @@ dkv_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUt
       mbar_init(B(B_QF + s), 1);
       mbar_init(B(B_QE + s), 1);
       mbar_init(B(B_IF + s), 64);
-      mbar_init(B(B_IE + s), 128);
+      mbar_init(B(B_IE + s), 256);
     }
     mbar_init(B(B_SF), 1);
-    mbar_init(B(B_SE), 128);
-    mbar_init(B(B_PF), 128);
+    mbar_init(B(B_SE), 256);
+    mbar_init(B(B_PF), 256);
     mbar_init(B(B_PE), 1);
     fence_mbar_init();
   }
@@ -416,27 +421,31 @@ dkv_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUt
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && total > 0) {
+    // whole warp runs the schedule; elect.sync picks the issuing lane
+    if (total > 0) {
       constexpr uint32_t id_s = idesc_bf16_f32(128, BR, 0, 0);
       constexpr uint32_t id_acc = idesc_bf16_f32(128, 128, 0, 1);
+      const uint64_t dk0 = sdesc_sw128(sb + OFF_K, 16, 1024), dv0 = sdesc_sw128(sb + OFF_V, 16, 1024);
+      const uint64_t dqs0 = sdesc_sw128(sb + OFF_Q, 16, 1024), ddos0 = sdesc_sw128(sb + OFF_DO, 16, 1024);
+      const uint64_t dqm0 = sdesc_sw128(sb + OFF_Q, QATOM, 1024), ddom0 = sdesc_sw128(sb + OFF_DO, QATOM, 1024);
+      const uint64_t dpt0 = sdesc_sw128(sb + OFF_PT, 16, 1024), ddst0 = sdesc_sw128(sb + OFF_DST, 16, 1024);
       auto issue_s = [&](int k) {
         const int s = k & 1;
         mbar_wait(B(B_QF + s), (k >> 1) & 1);
         tc_fence_after();
-        const uint32_t qb = sb + OFF_Q + s * QTILE, db = sb + OFF_DO + s * QTILE;
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
-          const uint32_t oa = (kk >> 2) * ATOM + (kk & 3) * 32, ob = (kk >> 2) * QATOM + (kk & 3) * 32;
-          umma_bf16(tmem + COL_S, sdesc_sw128(sb + OFF_K + oa, 16, 1024), sdesc_sw128(qb + ob, 16, 1024), id_s,
-                    kk > 0);
+          const uint32_t oa = ((kk >> 2) * ATOM + (kk & 3) * 32) >> 4;
+          const uint32_t ob = ((s * QTILE + (kk >> 2) * QATOM + (kk & 3) * 32)) >> 4;
+          umma_bf16_ws(tmem + COL_S, dk0 + oa, dqs0 + ob, id_s, kk > 0);
         }
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
-          const uint32_t oa = (kk >> 2) * ATOM + (kk & 3) * 32, ob = (kk >> 2) * QATOM + (kk & 3) * 32;
-          umma_bf16(tmem + COL_DP, sdesc_sw128(sb + OFF_V + oa, 16, 1024), sdesc_sw128(db + ob, 16, 1024), id_s,
-                    kk > 0);
+          const uint32_t oa = ((kk >> 2) * ATOM + (kk & 3) * 32) >> 4;
+          const uint32_t ob = ((s * QTILE + (kk >> 2) * QATOM + (kk & 3) * 32)) >> 4;
+          umma_bf16_ws(tmem + COL_DP, dv0 + oa, ddos0 + ob, id_s, kk > 0);
         }
-        umma_commit(B(B_SF));
+        umma_commit_ws(B(B_SF));
       };
       mbar_wait(B(B_KV), 0);
       issue_s(0);
@@ -446,19 +455,18 @@ dkv_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUt
         if (k + 1 < total) issue_s(k + 1);
         mbar_wait(B(B_PF), k & 1);
         tc_fence_after();
-        const uint32_t qb = sb + OFF_Q + s * QTILE, db = sb + OFF_DO + s * QTILE;
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) {  // K = 64 rows, 16 per MMA
-          umma_bf16(tmem + COL_DV, sdesc_sw128(sb + OFF_PT + kk * 32, 16, 1024),
-                    sdesc_sw128(db + kk * 2048, QATOM, 1024), id_acc, (k > 0 || kk > 0) ? 1u : 0u);
+          umma_bf16_ws(tmem + COL_DV, dpt0 + ((kk * 32) >> 4), ddom0 + ((s * QTILE + kk * 2048) >> 4), id_acc,
+                       (k > 0 || kk > 0) ? 1u : 0u);
         }
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) {
-          umma_bf16(tmem + COL_DK, sdesc_sw128(sb + OFF_DST + kk * 32, 16, 1024),
-                    sdesc_sw128(qb + kk * 2048, QATOM, 1024), id_acc, (k > 0 || kk > 0) ? 1u : 0u);
+          umma_bf16_ws(tmem + COL_DK, ddst0 + ((kk * 32) >> 4), dqm0 + ((s * QTILE + kk * 2048) >> 4), id_acc,
+                       (k > 0 || kk > 0) ? 1u : 0u);
         }
-        umma_commit(B(B_QE + s));
-        umma_commit(B(B_PE));
+        umma_commit_ws(B(B_QE + s));
+        umma_commit_ws(B(B_PE));
       }
     }
   } else if (warp == 2 || warp == 3) {
@@ -476,35 +484,36 @@ dkv_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUt
       reinterpret_cast<int*>(info)[(s * 3 + 2) * BR + r] = __ldg(visc + ci);
       mbar_arrive(B(B_IF + s));
     }
-  } else {
-    // softmax-gradient warps: thread j <-> key k0 + j <-> TMEM lane j
-    const int j = threadIdx.x - 128;
+  } else if (warp >= 4) {
+    // softmax-gradient warps: thread j <-> key k0 + j <-> TMEM lane j; two
+    // warps per lane quarter, each 32 of the 64 Q-row columns
+    const int hf = (warp - 4) >> 2;
+    const int j = (warp & 3) * 32 + lane;
     const int kj = k0 + j;
     const uint32_t tl = tmem + ((uint32_t)((warp & 3) * 32) << 16);
     const float sl2 = static_cast<float>(kLog2e / sqrt(static_cast<double>(D)));
     const float* info = reinterpret_cast<const float*>(smem + OFF_INFO);
     uint8_t* pt_gen = smem + OFF_PT;
     uint8_t* dst_gen = smem + OFF_DST;
+    const int cb = hf * 32;
     for (int k = 0; k < total; ++k) {
       const int s = k & 1;
       mbar_wait(B(B_SF), k & 1);
       tc_fence_after();
-      uint32_t sv[64], dp[64];
+      uint32_t sv[32], dp[32];
       __syncwarp();
-      tmem_ld32(tl + COL_S, sv);
-      tmem_ld32(tl + COL_S + 32, sv + 32);
-      tmem_ld32(tl + COL_DP, dp);
-      tmem_ld32(tl + COL_DP + 32, dp + 32);
+      tmem_ld32(tl + COL_S + cb, sv);
+      tmem_ld32(tl + COL_DP + cb, dp);
       tmem_wait_ld();
       tc_fence_before();
       mbar_arrive(B(B_SE));
       mbar_wait(B(B_IF + s), (k >> 1) & 1);
-      const float* l2 = info + (s * 3 + 0) * BR;
-      const float* dd = info + (s * 3 + 1) * BR;
-      const int* vv = reinterpret_cast<const int*>(info) + (s * 3 + 2) * BR;
-      uint32_t pp[32], pd[32];
+      const float* l2 = info + (s * 3 + 0) * BR + cb;
+      const float* dd = info + (s * 3 + 1) * BR + cb;
+      const int* vv = reinterpret_cast<const int*>(info) + (s * 3 + 2) * BR + cb;
+      uint32_t pp[16], pd[16];
 #pragma unroll
-      for (int c = 0; c < 64; c += 2) {
+      for (int c = 0; c < 32; c += 2) {
         const float p0 = (kj < vv[c]) ? fast_exp2(__uint_as_float(sv[c]) * sl2 - l2[c]) : 0.f;
         const float p1 = (kj < vv[c + 1]) ? fast_exp2(__uint_as_float(sv[c + 1]) * sl2 - l2[c + 1]) : 0.f;
         pp[c / 2] = pack_bf16x2(p0, p1);
@@ -513,9 +522,10 @@ dkv_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUt
       mbar_arrive(B(B_IE + s));
       if (k > 0) mbar_wait(B(B_PE), (k - 1) & 1);  // previous dV/dK MMAs done with P^T / dS^T
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        *reinterpret_cast<uint4*>(pt_gen + swz(j, q)) = make_uint4(pp[4 * q], pp[4 * q + 1], pp[4 * q + 2], pp[4 * q + 3]);
-        *reinterpret_cast<uint4*>(dst_gen + swz(j, q)) =
+      for (int q = 0; q < 4; ++q) {
+        *reinterpret_cast<uint4*>(pt_gen + swz(j, hf * 4 + q)) =
+            make_uint4(pp[4 * q], pp[4 * q + 1], pp[4 * q + 2], pp[4 * q + 3]);
+        *reinterpret_cast<uint4*>(dst_gen + swz(j, hf * 4 + q)) =
             make_uint4(pd[4 * q], pd[4 * q + 1], pd[4 * q + 2], pd[4 * q + 3]);
       }
       fence_proxy_async_smem();
@@ -523,18 +533,19 @@ dkv_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUt
       mbar_arrive(B(B_PF));
     }
     const bool valid = kj < nsel;
-    float4* dvr = reinterpret_cast<float4*>(dV + ((size_t)g * cap + kj) * D);
-    float4* dkr = reinterpret_cast<float4*>(dK + ((size_t)g * cap + kj) * D);
+    const int dcb = hf * 64;  // this thread's 64 head-dim columns of dK / dV
+    float4* dvr = reinterpret_cast<float4*>(dV + ((size_t)g * cap + kj) * D + dcb);
+    float4* dkr = reinterpret_cast<float4*>(dK + ((size_t)g * cap + kj) * D + dcb);
     if (total > 0) {
       mbar_wait(B(B_PE), (total - 1) & 1);
       tc_fence_after();
       const float scale = static_cast<float>(1.0 / sqrt(static_cast<double>(D)));
 #pragma unroll
-      for (int c4 = 0; c4 < 4; ++c4) {
+      for (int c4 = 0; c4 < 2; ++c4) {
         uint32_t a[32], b[32];
         __syncwarp();
-        tmem_ld32(tl + COL_DV + c4 * 32, a);
-        tmem_ld32(tl + COL_DK + c4 * 32, b);
+        tmem_ld32(tl + COL_DV + dcb + c4 * 32, a);
+        tmem_ld32(tl + COL_DK + dcb + c4 * 32, b);
         tmem_wait_ld();
         if (valid) {  // heads of the group reduce into the zero-initialised dK / dV
 #pragma unroll
@@ -615,11 +626,11 @@ extern "C" int omni_sparse_attn_bwd(const void* Q, const void* K_sel, const void
     attr = true;
   }
   const int n_tiles = capq / 128;
-  bwd::dq_kernel<<<n_tiles * n_q_heads, 256, bwd::dq::SMEM, st>>>(tq128, tdo128, tk, tv, rows, counts, lse2c, Dc,
+  bwd::dq_kernel<<<n_tiles * n_q_heads, 384, bwd::dq::SMEM, st>>>(tq128, tdo128, tk, tv, rows, counts, lse2c, Dc,
                                                                     visc, n_q_heads, rep, seq_len, cap, capq, n_tiles,
                                                                     dQ);
   if ((rc = omni_launch_check())) return rc;
-  bwd::dkv_kernel<<<dim3(cap / 128, n_kv_heads * rep), 256, bwd::dkv::SMEM, st>>>(tq64, tdo64, tk, tv, rows, counts,
+  bwd::dkv_kernel<<<dim3(cap / 128, n_kv_heads * rep), 384, bwd::dkv::SMEM, st>>>(tq64, tdo64, tk, tv, rows, counts,
                                                                             selected, sel_counts, lse2c, Dc, visc, rep,
                                                                             seq_len, cap, capq, dK_sel, dV_sel);
   return omni_launch_check();
