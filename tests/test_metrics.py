@@ -1,0 +1,141 @@
+"""Reporting helpers vs the reference (tests/golden/make_metrics_golden.py):
+OMNT tensor files, the analytic multiply-add / KV models, MetricsReport JSON
+schema v1, the oracle's recall; GPU recall (LSE identity) vs the oracle."""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle import metrics as om
+from paper_2511_12201_b200 import metrics as gm
+from paper_2511_12201_b200 import tensorfile as tf
+from paper_2511_12201_b200.errors import TensorFileError
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+GOLD = json.load(open(os.path.join(HERE, "golden", "metrics_golden.json")))
+
+
+def test_omnt_reads_reference_file_bit_exact(tmp_path):
+    m = tf.load_tensor(os.path.join(HERE, "golden", "omnt_ref.bin"))
+    np.testing.assert_array_equal(m, np.array(GOLD["omnt_matrix"]))
+    p = tmp_path / "x.omnt"
+    tf.save_tensor(p, m)
+    assert p.read_bytes() == open(os.path.join(HERE, "golden", "omnt_ref.bin"), "rb").read()
+
+
+def test_omnt_errors(tmp_path):
+    p = tmp_path / "bad.omnt"
+    with pytest.raises(TensorFileError):
+        tf.save_tensor(p, np.zeros(3))
+    with pytest.raises(TensorFileError):
+        tf.save_tensor(p, np.array([[np.nan]]))
+    p.write_bytes(b"OMNX" + b"\0" * 20)
+    with pytest.raises(TensorFileError):
+        tf.load_tensor(p)
+    tf.save_tensor(p, np.ones((2, 2)))
+    p.write_bytes(p.read_bytes()[:-8])
+    with pytest.raises(TensorFileError):
+        tf.load_tensor(p)
+    p.write_bytes(b"OMNT")
+    with pytest.raises(TensorFileError):
+        tf.load_tensor(p)
+
+
+def test_analytic_models_match_reference():
+    for case in GOLD["analytic_flops"]:
+        n, nv, d, act, b, blk, probe = case["args"]
+        f = gm.analytic_flops(n, nv, d, act, b, block_size=blk, probe_scores=probe)
+        assert (f.full, f.sparse, f.probe_overhead) == (case["full"], case["sparse"], case["probe_overhead"])
+        assert f.reduction == case["reduction"]
+    for case in GOLD["kv_reduction"]:
+        r = gm.kv_reduction(*case["args"])
+        assert r.resident_reduction == case["resident_reduction"]
+        assert r.fetch_reduction == case["fetch_reduction"]
+        assert r.predicted_vision_tokens == case["predicted_vision_tokens"]
+        assert r.predicted_vision_bytes == case["predicted_vision_bytes"]
+    with pytest.raises(ValueError):
+        gm.kv_reduction(10, 11, 8, 1, 1)
+    with pytest.raises(ValueError):
+        gm.analytic_flops(10, 8, 4, [1], 2, probe_scores=True)
+
+
+def test_oracle_recall_matches_reference():
+    for case in GOLD["recall"]:
+        r = om.attention_recall(np.array(case["map"]), case["selected"], case["active"])
+        assert r == pytest.approx(case["recall"], rel=1e-15)
+    assert om.attention_recall(np.ones((2, 2)), [0], [False, False]) == 1.0
+
+
+def test_report_json_round_trip():
+    r = gm.MetricsReport(mode="sparse", config={"tau": 0.08}, workload={"heads": 4}, flops_full=10, flops_sparse=3,
+                         flops_probe_overhead=1, flops_reduction=0.6, exponentials_full=5, exponentials_sparse=2,
+                         recall_per_head=[0.9, 1.0], recall_min=0.9, recall_flattest=0.82, flattest_retained_mass=8.2,
+                         flattest_total_mass=10.0, budget=7, flattest_head=1, lazy_query_fraction=0.5,
+                         sparsity_gap=None)
+    text = r.to_json()
+    assert json.loads(text)["schema_version"] == 1 and text.endswith("\n")
+    assert gm.MetricsReport.from_json(text) == r
+    d = r.to_dict()
+    d["schema_version"] = 2
+    with pytest.raises(ValueError):
+        gm.MetricsReport.from_dict(d)
+
+
+@pytest.mark.gpu
+def test_gpu_recall_matches_oracle():
+    """Per-head recall from the LSE identity (K4 over the selected keys and
+    over all keys) vs dense float64 maps of the oracle, C1-shaped workload."""
+    import torch
+
+    from oracle import pipeline as opipe
+    from oracle.workload import Spec, generate, round_bf16
+    from paper_2511_12201_b200.pipeline import SparsityConfig, sparse_prefill_device
+
+    Q, K, V = generate(Spec(heads=4, head_dim=128, n_vision=1984, n_text=64, seed=0))
+    Q, K, V = round_bf16(Q), round_bf16(K), round_bf16(V)
+    t = lambda x: torch.tensor(x, dtype=torch.bfloat16, device="cuda")
+    Qd, Kd, Vd = t(Q), t(K), t(V)
+    cfg = SparsityConfig()
+    res = sparse_prefill_device(Qd, Kd, Vd, 1984, cfg)
+    rec = gm.attention_recall_device(res, Qd, Kd, Vd).cpu().numpy()
+    ref = opipe.select(Q, K, 1984, 0, 0.08, 0.82, 256)
+    for h in range(4):
+        exp = om.head_recall(Q[h], K[h], ref.selected[h], ref.active[h])
+        assert abs(rec[h] - exp) < 2e-3, (h, rec[h], exp)
+    rep = gm.prefill_report(res, Qd, Kd, Vd, 1984, cfg)
+    assert rep.budget == ref.budget and rep.flattest_head == ref.flattest
+    assert gm.MetricsReport.from_json(rep.to_json()) == rep
+
+
+def _cli(args, tmp_path, name):
+    import subprocess
+    import sys
+
+    out = tmp_path / name
+    root = os.path.dirname(HERE)
+    r = subprocess.run([sys.executable, "-m", "paper_2511_12201_b200.cli", *args, "--out", str(out)], cwd=root,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    return out.read_text()
+
+
+@pytest.mark.gpu
+def test_cli_modes_and_determinism(tmp_path):
+    """SPEC run(): every mode writes schema-v1 JSON; identical flags + seed give
+    byte-identical reports (AC9); sparsity disabled -> no FLOPs saved."""
+    common = ["--heads", "4", "--dim", "128", "--nv", "1984", "--nt", "64", "--seed", "7"]
+    a = _cli(["--mode", "probe", *common], tmp_path, "a.json")
+    b = _cli(["--mode", "probe", *common], tmp_path, "b.json")
+    assert a == b
+    rep = gm.MetricsReport.from_json(a)
+    assert rep.schema_version == 1 and 0 < rep.budget <= 2048 and len(rep.recall_per_head) == 4
+    full = gm.MetricsReport.from_json(_cli(["--mode", "full", *common], tmp_path, "f.json"))
+    assert full.flops_reduction <= 0 and full.lazy_query_fraction == 0.0
+    sparse = gm.MetricsReport.from_json(_cli(["--mode", "sparse", *common], tmp_path, "s.json"))
+    assert sparse.recall_flattest >= 0.82 - 1e-9  # Eq. 5 guarantee on the exact score path
+    sweep = json.loads(_cli(["--mode", "sweep", "--tau", "0.08,0.12", "--p", "0.5,0.82", *common], tmp_path, "w.json"))
+    assert len(sweep) == 4
+    dec = gm.MetricsReport.from_json(_cli(["--mode", "decode", "--steps", "4", *common], tmp_path, "d.json"))
+    assert dec.decode["vision_tokens_fetched"] == dec.decode["predicted_vision_tokens"]  # AC6 exactness
