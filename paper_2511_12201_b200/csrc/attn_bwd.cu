@@ -102,7 +102,7 @@ constexpr uint32_t SMEM = OFF_TMEM + 16 + 1024;
 constexpr uint32_t COL_S = 0, COL_DP = 128, COL_DQ = 256;
 }  // namespace dq
 
-__global__ void __launch_bounds__(384, 1)
+__global__ void __launch_bounds__(576, 1)
 dq_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
           const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
           const int32_t* __restrict__ rows, const int32_t* __restrict__ counts, const float* __restrict__ lse2c,
@@ -140,8 +140,8 @@ dq_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
       mbar_init(B(B_VE + s), 1);
     }
     mbar_init(B(B_SF), 1);
-    mbar_init(B(B_SE), 256);
-    mbar_init(B(B_DSF), 256);
+    mbar_init(B(B_SE), 512);
+    mbar_init(B(B_DSF), 512);
     mbar_init(B(B_DSE), 1);
     fence_mbar_init();
   }
@@ -218,11 +218,13 @@ dq_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
         umma_commit_ws(B(B_DSE));
       }
     }
-  } else if (warp >= 4) {
-    // 8 warps: two per TMEM lane quarter, each thread 64 key columns of its row
-    const int hf = (warp - 4) >> 2;
+  } else if (warp >= 2) {
+    // 16 warps: four per TMEM lane quarter, each thread 32 key columns of its
+    // row. S and dP are read into registers first and released at once (the
+    // S / dP MMAs of the next key tile overlap this tile's dS math).
+    const int hf = (warp - 2) >> 2;  // column quarter 0..3
     const int i = (warp & 3) * 32 + lane;
-    const int cb = hf * 64;
+    const int cb = hf * 32;
     const bool valid = i < nrows;
     const size_t ci = crow0 + i;
     const int vis = valid ? __ldg(visc + ci) : 0;
@@ -234,32 +236,29 @@ dq_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
     for (int j = 0; j < nt; ++j) {
       mbar_wait(B(B_SF), j & 1);
       tc_fence_after();
-      if (j > 0) mbar_wait(B(B_DSE), (j - 1) & 1);  // dQ MMA of j-1 finished reading dS
-      const int lim = vis - j * 128;
-#pragma unroll
-      for (int c4 = 0; c4 < 2; ++c4) {
-        uint32_t s[32], p[32];
-        __syncwarp();
-        tmem_ld32(tl + COL_S + cb + c4 * 32, s);
-        tmem_ld32(tl + COL_DP + cb + c4 * 32, p);
-        tmem_wait_ld();
-        uint32_t pk[16];
-#pragma unroll
-        for (int c = 0; c < 32; c += 2) {
-          const int col = cb + c4 * 32 + c;
-          const float p0 = (col < lim) ? fast_exp2(__uint_as_float(s[c]) * sl2 - l2) : 0.f;
-          const float p1 = (col + 1 < lim) ? fast_exp2(__uint_as_float(s[c + 1]) * sl2 - l2) : 0.f;
-          pk[c / 2] = pack_bf16x2(p0 * (__uint_as_float(p[c]) - Dv), p1 * (__uint_as_float(p[c + 1]) - Dv));
-        }
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int chunk = hf * 8 + c4 * 4 + q;  // 16-byte chunk index along keys (0..15)
-          *reinterpret_cast<uint4*>(ds_gen + (chunk >> 3) * ATOM + swz(i, chunk & 7)) =
-              make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
-        }
-      }
+      uint32_t s[32], p[32];
+      __syncwarp();
+      tmem_ld32(tl + COL_S + cb, s);
+      tmem_ld32(tl + COL_DP + cb, p);
+      tmem_wait_ld();
       tc_fence_before();
-      mbar_arrive(B(B_SE));
+      mbar_arrive(B(B_SE));  // S / dP of this tile consumed: the next tile's MMAs may overwrite them
+      const int lim = vis - j * 128;
+      uint32_t pk[16];
+#pragma unroll
+      for (int c = 0; c < 32; c += 2) {
+        const int col = cb + c;
+        const float p0 = (col < lim) ? fast_exp2(__uint_as_float(s[c]) * sl2 - l2) : 0.f;
+        const float p1 = (col + 1 < lim) ? fast_exp2(__uint_as_float(s[c + 1]) * sl2 - l2) : 0.f;
+        pk[c / 2] = pack_bf16x2(p0 * (__uint_as_float(p[c]) - Dv), p1 * (__uint_as_float(p[c + 1]) - Dv));
+      }
+      if (j > 0) mbar_wait(B(B_DSE), (j - 1) & 1);  // dQ MMA of j-1 finished reading dS
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int chunk = hf * 4 + q;  // 16-byte chunk index along keys (0..15)
+        *reinterpret_cast<uint4*>(ds_gen + (chunk >> 3) * ATOM + swz(i, chunk & 7)) =
+            make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+      }
       fence_proxy_async_smem();
       mbar_arrive(B(B_DSF));
     }
@@ -269,19 +268,15 @@ dq_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
       const float scale = static_cast<float>(1.0 / sqrt(static_cast<double>(D)));
       const int pos = valid ? __ldg(rows + (size_t)h * N + r0 + i) : 0;
       float4* dst = reinterpret_cast<float4*>(dQ + ((size_t)h * N + pos) * D + cb);
+      uint32_t o[32];
+      __syncwarp();
+      tmem_ld32(tl + COL_DQ + cb, o);
+      tmem_wait_ld();
+      if (valid) {
 #pragma unroll
-      for (int c4 = 0; c4 < 2; ++c4) {
-        uint32_t o[32];
-        __syncwarp();
-        tmem_ld32(tl + COL_DQ + cb + c4 * 32, o);
-        tmem_wait_ld();
-        if (valid) {
-#pragma unroll
-          for (int q = 0; q < 8; ++q)
-            dst[c4 * 8 + q] = make_float4(__uint_as_float(o[4 * q]) * scale, __uint_as_float(o[4 * q + 1]) * scale,
-                                          __uint_as_float(o[4 * q + 2]) * scale,
-                                          __uint_as_float(o[4 * q + 3]) * scale);
-        }
+        for (int q = 0; q < 8; ++q)
+          dst[q] = make_float4(__uint_as_float(o[4 * q]) * scale, __uint_as_float(o[4 * q + 1]) * scale,
+                               __uint_as_float(o[4 * q + 2]) * scale, __uint_as_float(o[4 * q + 3]) * scale);
       }
     }
   }
@@ -626,7 +621,7 @@ extern "C" int omni_sparse_attn_bwd(const void* Q, const void* K_sel, const void
     attr = true;
   }
   const int n_tiles = capq / 128;
-  bwd::dq_kernel<<<n_tiles * n_q_heads, 384, bwd::dq::SMEM, st>>>(tq128, tdo128, tk, tv, rows, counts, lse2c, Dc,
+  bwd::dq_kernel<<<n_tiles * n_q_heads, 576, bwd::dq::SMEM, st>>>(tq128, tdo128, tk, tv, rows, counts, lse2c, Dc,
                                                                     visc, n_q_heads, rep, seq_len, cap, capq, n_tiles,
                                                                     dQ);
   if ((rc = omni_launch_check())) return rc;
