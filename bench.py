@@ -551,6 +551,28 @@ def run_ours(args):
                               "work_ratio": work_flops(r2, HKV) / (4.0 * D * HQ * n * (n + 1) / 2)})
                 del Q2, K2, V2, O2, r2
             line["knob_sweep"] = sweep
+        log("size sweep")
+        # ----- C2 (32K) and C3 upper size (128K) at the reference defaults
+        if not args.no_knobs and not args.no_dense:
+            sizes = []
+            for n2 in (32768, 131072):
+                try:
+                    Q2, K2, V2 = generate_device(HQ, HKV, D, n2 - N_TEXT, N_TEXT, seed=0, lazy_fraction=args.lazy)
+                    O2 = torch.empty_like(Q2)
+                    st2 = lambda: sparse_prefill_device(Q2, K2, V2, n2 - N_TEXT, cfg, out=O2)
+                    r2 = st2()
+                    ms2 = time_cuda(st2, args.steps, 2)
+                    dn = dense_baselines(Q2, K2, V2, max(3, args.steps // 2), 2)
+                    sizes.append({"tokens": n2, "ms_per_step": ms2, "tok_s": n2 / (ms2 / 1e3),
+                                  "dense_fastest": dn.get("fastest"), "dense_ms": dn.get("fastest_ms"),
+                                  "speedup_vs_dense_fa": (dn["fastest_ms"] / ms2) if "fastest_ms" in dn else None,
+                                  "budget": int(r2.selection.info[0]),
+                                  "work_ratio": work_flops(r2, HKV) / (4.0 * D * HQ * n2 * (n2 + 1) / 2)})
+                    del Q2, K2, V2, O2, r2
+                    torch.cuda.empty_cache()
+                except Exception as e:  # noqa: BLE001
+                    sizes.append({"tokens": n2, "error": str(e)[:200]})
+            line["size_sweep"] = sizes
         log("e2e")
         # ----- end-to-end through the public API with host buffers
         if not args.no_e2e:
