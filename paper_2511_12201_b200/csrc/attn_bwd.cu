@@ -18,6 +18,8 @@
 //         dV += P^T dO, dK += dS^T Q (TMEM accumulators). GQA accumulation over
 //         the group's Q heads happens inside one CTA (deterministic).
 #include <math.h>
+#include <stdlib.h>
+#include <string.h>
 
 #include "common.cuh"
 
@@ -563,6 +565,252 @@ dkv_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUt
   }
 }
 
+// ------------------------------------------------------------------ dkv v2
+// dkv with 128-row Q tiles and P^T / dS^T kept in TMEM. Per (key tile, Q
+// tile k): S^T = K Q^T and dP^T = V dO^T (SS, M = 128 keys, N = 128 rows) into
+// TMEM; 16 gradient warps (four per lane quarter, 32 row columns each) read
+// their S^T / dP^T columns, release them, and write P^T and dS^T as bf16
+// pairs over their own dP^T columns; dV += P^T dO and dK += dS^T Q are
+// TS-mode MMAs (A from TMEM). No P^T / dS^T round trip through shared memory
+// (the old kernel's bandwidth limit), and S^T(k+1) is computed while tile k's
+// gradients are formed (only dP^T(k+1) waits for dV / dK(k)).
+namespace dkv2 {
+constexpr int BR = 128;
+constexpr uint32_t OFF_K = 0, OFF_V = TILE, OFF_Q = 2 * TILE, OFF_DO = 4 * TILE;  // Q, dO: 2 stages each
+constexpr uint32_t OFF_INFO = 6 * TILE;                                           // [2][3][128]
+constexpr uint32_t OFF_BAR = OFF_INFO + 2 * 3 * BR * 4;
+enum { B_KV = 0, B_QF = 1, B_QE = 3, B_IF = 5, B_IE = 7, B_SF = 9, B_SE = 10, B_PF = 11, B_PE = 12, B_N = 13 };
+constexpr uint32_t OFF_TMEM = OFF_BAR + 8 * B_N;
+constexpr uint32_t SMEM = OFF_TMEM + 16 + 1024;
+constexpr uint32_t COL_S = 0, COL_DP = 128, COL_DV = 256, COL_DK = 384;
+constexpr int NTHREADS = 640;  // TMA, MMA, 2 row-info warps, 16 gradient warps
+}  // namespace dkv2
+
+__global__ void __launch_bounds__(dkv2::NTHREADS, 1)
+dkv2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
+            const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
+            const int32_t* __restrict__ rows, const int32_t* __restrict__ counts, const int32_t* __restrict__ sel,
+            const int32_t* __restrict__ sel_counts, const float* __restrict__ lse2c, const float* __restrict__ Dc,
+            const int32_t* __restrict__ visc, int rep, int N, int cap, int capq, float* __restrict__ dK,
+            float* __restrict__ dV) {
+  using namespace dkv2;
+  extern __shared__ uint8_t smem_raw[];
+  // CTA = (key tile t, group g, Q head g*rep + rs), as dkv_kernel.
+  const int t = blockIdx.x, g = blockIdx.y / rep, rs = blockIdx.y % rep;
+  const int nsel = __ldg(sel_counts + g);
+  const int k0 = t * 128;
+  if (k0 >= nsel) return;
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sb = smem_u32(smem);
+  const uint32_t bar = sb + OFF_BAR;
+  auto B = [&](int i) { return bar + 8u * i; };
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + OFF_TMEM);
+  __shared__ int s_first, s_total;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int h = g * rep + rs;
+  if (threadIdx.x == 0) {
+    const int first_key = __ldg(sel + (size_t)g * N + k0);
+    const int cnt = __ldg(counts + h);
+    // first compact row whose position >= first_key (it sees key k0)
+    const int32_t* rh = rows + (size_t)h * N;
+    int lo = 0, hi = cnt;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (__ldg(rh + mid) < first_key) lo = mid + 1; else hi = mid;
+    }
+    s_first = lo / BR;
+    s_total = max(0, (cnt + BR - 1) / BR - lo / BR);
+    tma_prefetch_desc(&tm_q);
+    tma_prefetch_desc(&tm_do);
+    tma_prefetch_desc(&tm_k);
+    tma_prefetch_desc(&tm_v);
+    mbar_init(B(B_KV), 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(B(B_QF + s), 1);
+      mbar_init(B(B_QE + s), 1);
+      mbar_init(B(B_IF + s), 64);
+      mbar_init(B(B_IE + s), 512);
+    }
+    mbar_init(B(B_SF), 1);
+    mbar_init(B(B_SE), 512);
+    mbar_init(B(B_PF), 512);
+    mbar_init(B(B_PE), 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) {
+    tmem_alloc(smem_u32(tmem_slot), 512);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int total = s_total, first = s_first;
+
+  if (warp == 0) {
+    if (lane == 0 && total > 0) {
+      mbar_expect_tx(B(B_KV), 2 * TILE);
+      const int kr = g * cap + k0;
+      tma_load_2d(sb + OFF_K, &tm_k, B(B_KV), 0, kr);
+      tma_load_2d(sb + OFF_K + ATOM, &tm_k, B(B_KV), 64, kr);
+      tma_load_2d(sb + OFF_V, &tm_v, B(B_KV), 0, kr);
+      tma_load_2d(sb + OFF_V + ATOM, &tm_v, B(B_KV), 64, kr);
+      for (int k = 0; k < total; ++k) {
+        const int s = k & 1;
+        const int row = h * capq + (first + k) * BR;
+        if (k >= 2) mbar_wait(B(B_QE + s), ((k >> 1) - 1) & 1);
+        mbar_expect_tx(B(B_QF + s), 2 * TILE);
+        tma_load_2d(sb + OFF_Q + s * TILE, &tm_q, B(B_QF + s), 0, row);
+        tma_load_2d(sb + OFF_Q + s * TILE + ATOM, &tm_q, B(B_QF + s), 64, row);
+        tma_load_2d(sb + OFF_DO + s * TILE, &tm_do, B(B_QF + s), 0, row);
+        tma_load_2d(sb + OFF_DO + s * TILE + ATOM, &tm_do, B(B_QF + s), 64, row);
+      }
+    }
+  } else if (warp == 1) {
+    // whole warp runs the schedule; elect.sync picks the issuing lane
+    if (total > 0) {
+      constexpr uint32_t id_s = idesc_bf16_f32(128, BR, 0, 0);
+      constexpr uint32_t id_acc = idesc_bf16_f32(128, 128, 0, 1);
+      const uint64_t dk0 = sdesc_sw128(sb + OFF_K, 16, 1024), dv0 = sdesc_sw128(sb + OFF_V, 16, 1024);
+      const uint64_t dq0 = sdesc_sw128(sb + OFF_Q, 16, 1024), ddo0 = sdesc_sw128(sb + OFF_DO, 16, 1024);
+      const uint64_t dqm0 = sdesc_sw128(sb + OFF_Q, ATOM, 1024), ddom0 = sdesc_sw128(sb + OFF_DO, ATOM, 1024);
+      auto issue_st = [&](int k) {  // S^T(k) = K Q(k)^T -> COL_S
+        const int s = k & 1;
+        mbar_wait(B(B_QF + s), (k >> 1) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t off = ((kk >> 2) * ATOM + (kk & 3) * 32) >> 4;
+          umma_bf16_ws(tmem + COL_S, dk0 + off, dq0 + ((s * TILE) >> 4) + off, id_s, kk > 0);
+        }
+      };
+      auto issue_dpt = [&](int k) {  // dP^T(k) = V dO(k)^T -> COL_DP
+        const int s = k & 1;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t off = ((kk >> 2) * ATOM + (kk & 3) * 32) >> 4;
+          umma_bf16_ws(tmem + COL_DP, dv0 + off, ddo0 + ((s * TILE) >> 4) + off, id_s, kk > 0);
+        }
+        umma_commit_ws(B(B_SF));
+      };
+      mbar_wait(B(B_KV), 0);
+      issue_st(0);
+      issue_dpt(0);
+      for (int k = 0; k < total; ++k) {
+        const int s = k & 1;
+        mbar_wait(B(B_SE), k & 1);  // S^T(k), dP^T(k) read by every gradient thread
+        tc_fence_after();
+        if (k + 1 < total) issue_st(k + 1);
+        mbar_wait(B(B_PF), k & 1);  // P^T(k), dS^T(k) in TMEM
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {  // K = 128 rows, 16 per MMA
+          const uint32_t ac = COL_DP + 32u * (kk >> 1) + 8u * (kk & 1);
+          umma_bf16_ts_ws(tmem + COL_DV, tmem + ac, ddom0 + ((s * TILE + kk * 2048) >> 4), id_acc,
+                          (k > 0 || kk > 0) ? 1u : 0u);
+        }
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t ac = COL_DP + 32u * (kk >> 1) + 16u + 8u * (kk & 1);
+          umma_bf16_ts_ws(tmem + COL_DK, tmem + ac, dqm0 + ((s * TILE + kk * 2048) >> 4), id_acc,
+                          (k > 0 || kk > 0) ? 1u : 0u);
+        }
+        umma_commit_ws(B(B_QE + s));
+        umma_commit_ws(B(B_PE));
+        if (k + 1 < total) issue_dpt(k + 1);  // after dV / dK(k): they read the dP^T region
+      }
+    }
+  } else if (warp == 2 || warp == 3) {
+    // row-info loader: lse2 / D / vis of the 128 rows of each Q tile -> smem ring
+    const int r = threadIdx.x - 64;  // rows r and r + 64
+    float* info = reinterpret_cast<float*>(smem + OFF_INFO);
+    for (int k = 0; k < total; ++k) {
+      const int s = k & 1;
+      if (k >= 2) mbar_wait(B(B_IE + s), ((k >> 1) - 1) & 1);
+      for (int rr = r; rr < BR; rr += 64) {
+        const size_t ci = (size_t)h * capq + (first + k) * BR + rr;
+        info[(s * 3 + 0) * BR + rr] = __ldg(lse2c + ci);
+        info[(s * 3 + 1) * BR + rr] = __ldg(Dc + ci);
+        reinterpret_cast<int*>(info)[(s * 3 + 2) * BR + rr] = __ldg(visc + ci);
+      }
+      mbar_arrive(B(B_IF + s));
+    }
+  } else {
+    // gradient warps: thread j <-> key k0 + j <-> TMEM lane j; four warps per
+    // lane quarter, each 32 of the 128 Q-row columns
+    const int cq = (warp - 4) >> 2;
+    const int j = (warp & 3) * 32 + lane;
+    const int kj = k0 + j;
+    const uint32_t tl = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+    const float sl2 = static_cast<float>(kLog2e / sqrt(static_cast<double>(D)));
+    const float* info = reinterpret_cast<const float*>(smem + OFF_INFO);
+    const int cb = cq * 32;
+    for (int k = 0; k < total; ++k) {
+      const int s = k & 1;
+      mbar_wait(B(B_SF), k & 1);
+      tc_fence_after();
+      uint32_t sv[32], dp[32];
+      __syncwarp();
+      tmem_ld32(tl + COL_S + cb, sv);
+      tmem_ld32(tl + COL_DP + cb, dp);
+      tmem_wait_ld();
+      tc_fence_before();
+      mbar_arrive(B(B_SE));
+      mbar_wait(B(B_IF + s), (k >> 1) & 1);
+      const float* l2 = info + (s * 3 + 0) * BR + cb;
+      const float* dd = info + (s * 3 + 1) * BR + cb;
+      const int* vv = reinterpret_cast<const int*>(info) + (s * 3 + 2) * BR + cb;
+      uint32_t pp[16], pd[16];
+#pragma unroll
+      for (int c = 0; c < 32; c += 2) {
+        const float p0 = (kj < vv[c]) ? fast_exp2(__uint_as_float(sv[c]) * sl2 - l2[c]) : 0.f;
+        const float p1 = (kj < vv[c + 1]) ? fast_exp2(__uint_as_float(sv[c + 1]) * sl2 - l2[c + 1]) : 0.f;
+        pp[c / 2] = pack_bf16x2(p0, p1);
+        pd[c / 2] = pack_bf16x2(p0 * (__uint_as_float(dp[c]) - dd[c]), p1 * (__uint_as_float(dp[c + 1]) - dd[c + 1]));
+      }
+      mbar_arrive(B(B_IE + s));
+      // P^T / dS^T over this thread's own (already read) dP^T columns; dV / dK(k-1)
+      // finished reading the region before dP^T(k) was computed (in-order tensor pipe)
+      __syncwarp();
+      tmem_st16(tl + COL_DP + cb, pp);
+      tmem_st16(tl + COL_DP + cb + 16, pd);
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(B(B_PF));
+    }
+    const bool valid = kj < nsel;
+    const int dcb = cq * 32;  // this thread's 32 head-dim columns of dK / dV
+    float4* dvr = reinterpret_cast<float4*>(dV + ((size_t)g * cap + kj) * D + dcb);
+    float4* dkr = reinterpret_cast<float4*>(dK + ((size_t)g * cap + kj) * D + dcb);
+    if (total > 0) {
+      mbar_wait(B(B_PE), (total - 1) & 1);
+      tc_fence_after();
+      const float scale = static_cast<float>(1.0 / sqrt(static_cast<double>(D)));
+      uint32_t a[32], b[32];
+      __syncwarp();
+      tmem_ld32(tl + COL_DV + dcb, a);
+      tmem_ld32(tl + COL_DK + dcb, b);
+      tmem_wait_ld();
+      if (valid) {  // heads of the group reduce into the zero-initialised dK / dV
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          red_add_v4(dvr + q, __uint_as_float(a[4 * q]), __uint_as_float(a[4 * q + 1]), __uint_as_float(a[4 * q + 2]),
+                     __uint_as_float(a[4 * q + 3]));
+          red_add_v4(dkr + q, __uint_as_float(b[4 * q]) * scale, __uint_as_float(b[4 * q + 1]) * scale,
+                     __uint_as_float(b[4 * q + 2]) * scale, __uint_as_float(b[4 * q + 3]) * scale);
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    __syncwarp();
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
 }  // namespace bwd
 }  // namespace omni
 
@@ -625,8 +873,26 @@ extern "C" int omni_sparse_attn_bwd(const void* Q, const void* K_sel, const void
                                                                     visc, n_q_heads, rep, seq_len, cap, capq, n_tiles,
                                                                     dQ);
   if ((rc = omni_launch_check())) return rc;
-  bwd::dkv_kernel<<<dim3(cap / 128, n_kv_heads * rep), 384, bwd::dkv::SMEM, st>>>(tq64, tdo64, tk, tv, rows, counts,
-                                                                            selected, sel_counts, lse2c, Dc, visc, rep,
-                                                                            seq_len, cap, capq, dK_sel, dV_sel);
+  // dkv implementation: TMEM-resident P^T / dS^T kernel by default;
+  // OMNI_BWD_DKV=v1 selects the shared-memory P^T kernel.
+  static const bool dkv_v1 = [] {
+    const char* e = getenv("OMNI_BWD_DKV");
+    return e && strcmp(e, "v1") == 0;
+  }();
+  if (dkv_v1) {
+    bwd::dkv_kernel<<<dim3(cap / 128, n_kv_heads * rep), 384, bwd::dkv::SMEM, st>>>(
+        tq64, tdo64, tk, tv, rows, counts, selected, sel_counts, lse2c, Dc, visc, rep, seq_len, cap, capq, dK_sel,
+        dV_sel);
+  } else {
+    static bool attr2 = false;
+    if (!attr2) {
+      OMNI_CUDA_TRY(cudaFuncSetAttribute(bwd::dkv2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)bwd::dkv2::SMEM));
+      attr2 = true;
+    }
+    bwd::dkv2_kernel<<<dim3(cap / 128, n_kv_heads * rep), bwd::dkv2::NTHREADS, bwd::dkv2::SMEM, st>>>(
+        tq128, tdo128, tk, tv, rows, counts, selected, sel_counts, lse2c, Dc, visc, rep, seq_len, cap, capq, dK_sel,
+        dV_sel);
+  }
   return omni_launch_check();
 }
