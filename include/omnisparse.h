@@ -142,6 +142,12 @@ int omni_gather_rows(const void* src, int dtype, int n_groups, int src_rows, int
                      int idx_stride, const int32_t* counts, int count_const, void* dst, int dst_rows, int pad_rows,
                      void* stream);
 
+/* Inverse of omni_gather_rows: dst[g, idx[g, r]] = src[g, r] for
+ * r < counts[g] (device i32 [G]); other dst rows are untouched. Used to put
+ * compacted key gradients back at their original positions. */
+int omni_scatter_rows(const void* src, int dtype, int n_groups, int src_rows, int head_dim, const int32_t* idx,
+                      int idx_stride, const int32_t* counts, void* dst, int dst_rows, void* stream);
+
 /* ---------------------------------------------------------------- K4
  * Gathered sparse flash-attention forward (tcgen05 + TMEM + TMA).
  * Replaces sparse_head_attention (prefill.py:89-122) for every Q head:

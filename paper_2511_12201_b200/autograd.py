@@ -49,13 +49,11 @@ class SparseAttentionFn(torch.autograd.Function):
         n = Qb.shape[1]
         dQ, dKs, dVs, dVsink = ops.sparse_attn_bwd(Qb, K_sel, V_sel, O, dO.to(torch.bfloat16).contiguous(), lse,
                                                    plan.rows, plan.counts, plan.selected, plan.sel_counts)
-        dK = torch.zeros(hkv, n, Qb.shape[2], device=Qb.device, dtype=torch.float32)
-        dV = torch.zeros_like(dK)
-        counts = plan.sel_counts.tolist()
-        for g in range(hkv):  # scatter the compacted key gradients back to original positions
-            idx = plan.selected[g, : counts[g]].long()
-            dK[g].index_copy_(0, idx, dKs[g, : counts[g]])
-            dV[g].index_copy_(0, idx, dVs[g, : counts[g]])
+        # compacted key gradients back to their original positions (device
+        # counts: no host round trip)
+        dK = ops.scatter_rows(dKs, plan.selected, plan.sel_counts,
+                              torch.zeros(hkv, n, Qb.shape[2], device=Qb.device, dtype=torch.float32))
+        dV = ops.scatter_rows(dVs, plan.selected, plan.sel_counts, torch.zeros_like(dK))
         dV[:, plan.sink_index] += dVsink
         qd, kd, vd = ctx.dtypes
         return dQ.to(qd), dK.to(kd), dV.to(vd), None

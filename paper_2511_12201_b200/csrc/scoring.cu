@@ -485,6 +485,25 @@ __global__ void __launch_bounds__(256) gather_rows_kernel(const uint8_t* __restr
   }
 }
 
+// dst[g, idx[g, r]] = src[g, r] for r < counts[g] (the inverse of the gather:
+// compacted key gradients back to original positions), 16-byte lane copies.
+__global__ void __launch_bounds__(256) scatter_rows_kernel(const uint8_t* __restrict__ src, int src_rows,
+                                                           int row_bytes, const int32_t* __restrict__ idx,
+                                                           int idx_stride, const int32_t* __restrict__ counts,
+                                                           uint8_t* __restrict__ dst, int dst_rows) {
+  const int g = blockIdx.y;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int cnt = min(__ldg(counts + g), src_rows);
+  const int chunks = row_bytes >> 4;
+  for (int r = blockIdx.x * 8 + warp; r < cnt; r += gridDim.x * 8) {
+    const int d = __ldg(idx + (size_t)g * idx_stride + r);
+    if (d < 0 || d >= dst_rows) continue;
+    const uint4* s = reinterpret_cast<const uint4*>(src + ((size_t)g * src_rows + r) * row_bytes);
+    uint4* o = reinterpret_cast<uint4*>(dst + ((size_t)g * dst_rows + d) * row_bytes);
+    for (int c = lane; c < chunks; c += 32) o[c] = __ldg(s + c);
+  }
+}
+
 }  // namespace omni
 
 using namespace omni;
@@ -586,5 +605,20 @@ extern "C" int omni_gather_rows(const void* src, int dtype, int n_groups, int sr
   gather_rows_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
       static_cast<const uint8_t*>(src), src_rows, row_bytes, idx, idx_stride, counts, count_const,
       static_cast<uint8_t*>(dst), dst_rows, pad_rows);
+  return omni_launch_check();
+}
+
+extern "C" int omni_scatter_rows(const void* src, int dtype, int n_groups, int src_rows, int head_dim,
+                                 const int32_t* idx, int idx_stride, const int32_t* counts, void* dst, int dst_rows,
+                                 void* stream) {
+  const int esz = dtype == OMNI_DTYPE_BF16 ? 2 : 4;
+  const int row_bytes = head_dim * esz;
+  OMNI_CHECK(row_bytes % 16 == 0, OMNI_E_SHAPE, "row bytes must be a multiple of 16");
+  OMNI_CHECK(counts != nullptr, OMNI_E_PARAM, "scatter needs device counts");
+  if (n_groups == 0 || src_rows == 0) return OMNI_OK;
+  dim3 grid(min(nblocks(src_rows, 8), 1024), n_groups);
+  scatter_rows_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const uint8_t*>(src), src_rows, row_bytes, idx, idx_stride, counts, static_cast<uint8_t*>(dst),
+      dst_rows);
   return omni_launch_check();
 }

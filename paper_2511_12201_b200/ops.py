@@ -178,6 +178,18 @@ def gather_rows(src: torch.Tensor, idx: torch.Tensor, counts: torch.Tensor | int
     return out
 
 
+def scatter_rows(src: torch.Tensor, idx: torch.Tensor, counts: torch.Tensor, out: torch.Tensor) -> torch.Tensor:
+    """out[g, idx[g, r]] = src[g, r] for r < counts[g] (inverse of gather_rows)."""
+    _cuda3(src, "src")
+    _cuda3(out, "out")
+    g, rows, d = src.shape
+    if out.dtype != src.dtype or out.shape[0] != g or out.shape[2] != d:
+        raise ShapeError("scatter target must match the source dtype, groups and row width")
+    _lib.call("omni_scatter_rows", _p(src), _dtype(src), g, rows, d, _p(idx), idx.shape[-1], _p(counts), _p(out),
+              out.shape[1], _stream())
+    return out
+
+
 # ----------------------------------------------------------------------- K4
 def sparse_attn_fwd(Q, K_sel, V_sel, V, rows, counts, selected, sel_counts, sink_index: int,
                     O: torch.Tensor, lse: torch.Tensor | None = None):
