@@ -203,6 +203,23 @@ int omni_decode_step(const void* q, const void* vision_k, const void* vision_v, 
                      int n_kv_heads, int head_dim, int vcap, int acap, double tau, int preserve_first_head,
                      const uint8_t* flags_override, uint8_t* flags, float* out, void* workspace, void* stream);
 
+/* K7 for a serving batch of ragged sequences: as omni_decode_step, but the
+ * text and answer segment lengths are per sequence (device i32 [B]
+ * text_len <= tcap, answer_len <= acap; text_k/v [B, Hkv, tcap, d]).
+ * The reference keeps one growable list per head (decode.py:111-121); a
+ * batch of sequences admitted at different times needs per-sequence lengths.
+ * status i32 (device, required) receives this step's degenerate-context flag
+ * (1: a lazy head had no text and no answer key, decode.py:152-153) without a
+ * host synchronisation. Workspace: omni_decode_workspace(batch, Hq, vcap,
+ * tcap, acap, d).                                                          */
+int omni_decode_step_varlen(const void* q, const void* vision_k, const void* vision_v, const int32_t* vision_len,
+                            const void* text_k, const void* text_v, const int32_t* text_len, int tcap,
+                            const void* answer_k, const void* answer_v, const int32_t* answer_len,
+                            const double* k_lazy, const double* k_act, int batch, int n_q_heads, int n_kv_heads,
+                            int head_dim, int vcap, int acap, double tau, int preserve_first_head,
+                            const uint8_t* flags_override, uint8_t* flags, float* out, void* workspace,
+                            int32_t* status, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -48,6 +48,9 @@ SIGNATURES = {
     "omni_decode_workspace": (_c_size, [_c_int, _c_int, _c_int, _c_int, _c_int, _c_int]),
     "omni_decode_step": (_c_int, [_p, _p, _p, _p, _p, _p, _c_int, _p, _p, _c_int, _p, _p, _c_int, _c_int,
                                   _c_int, _c_int, _c_int, _c_int, _c_double, _c_int, _p, _p, _p, _p, _p]),
+    "omni_decode_step_varlen": (_c_int, [_p, _p, _p, _p, _p, _p, _p, _c_int, _p, _p, _p, _p, _p, _c_int, _c_int,
+                                         _c_int, _c_int, _c_int, _c_int, _c_double, _c_int, _p, _p, _p, _p, _p,
+                                         _p]),
 }
 
 _lib = None

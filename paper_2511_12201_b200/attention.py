@@ -88,3 +88,66 @@ class AttentionWorkload:
             return torch.stack([torch.as_tensor(np.asarray(x) if not isinstance(x, torch.Tensor) else x)
                                 .to(device=device, dtype=dtype) for x in xs]).contiguous()
         return pack(self.queries), pack(self.keys), pack(self.values)
+
+
+@dataclass
+class MultiheadOutput:
+    """reference attention.py:87-91: per-head outputs, their horizontal
+    concatenation (optionally projected) and, on request, the maps."""
+
+    head_outputs: torch.Tensor        # [Hq, N, d]
+    concatenated: torch.Tensor        # [N, Hq * d] or [N, out] after the projection
+    attention: list | None = None
+
+
+def concat_heads(outputs: torch.Tensor, output_proj: torch.Tensor | None = None) -> torch.Tensor:
+    """Head outputs [Hq, N, d] concatenated in head order ([N, Hq * d],
+    attention.py:131) and multiplied by ``output_proj`` [Hq * d, out] when
+    given (:132-133). fp32 on the GPU (cuBLAS), whatever the head dtype."""
+    hq, n, d = outputs.shape
+    concat = outputs.float().transpose(0, 1).reshape(n, hq * d)
+    if output_proj is None:
+        return concat
+    W = torch.as_tensor(output_proj, device=outputs.device, dtype=torch.float32)
+    if W.shape[0] != hq * d:
+        raise ShapeError(f"output projection has {W.shape[0]} rows, concatenation has {hq * d} columns")
+    return concat @ W
+
+
+def full_multihead(w: AttentionWorkload, causal: bool = True, output_proj=None, keep_attention: bool = False
+                   ) -> MultiheadOutput:
+    """Exact multi-head attention over a workload (attention.py:111-134).
+
+    Causal: K4 (the sparse kernel) with every row active and the identity key
+    selection is dense causal attention. Non-causal runs cuDNN SDPA (a
+    comparator, not part of the hot path). ``keep_attention`` materialises
+    the fp32 maps (validation sizes only)."""
+    from . import ops
+
+    Q, K, V = w.device_tensors()
+    hq, n, d = Q.shape
+    hkv = K.shape[0]
+    rep = hq // hkv
+    if causal:
+        ident = torch.arange(n, device=Q.device, dtype=torch.int32).repeat(hkv, 1).contiguous()
+        cnt = torch.full((hkv,), n, device=Q.device, dtype=torch.int32)
+        rows = torch.arange(n, device=Q.device, dtype=torch.int32).repeat(hq, 1).contiguous()
+        rcnt = torch.full((hq,), n, device=Q.device, dtype=torch.int32)
+        cap = ops.round_up(n, ops.TILE)
+        O = torch.empty_like(Q)
+        ops.sparse_attn_fwd(Q, ops.gather_rows(K, ident, cnt, cap, ops.TILE),
+                            ops.gather_rows(V, ident, cnt, cap, ops.TILE), V, rows, rcnt, ident, cnt, 0, O, None)
+    else:
+        Ke, Ve = K.repeat_interleave(rep, dim=0), V.repeat_interleave(rep, dim=0)
+        O = torch.nn.functional.scaled_dot_product_attention(Q[None], Ke[None], Ve[None])[0]
+    maps = None
+    if keep_attention:
+        if n > 8192:
+            raise ShapeError("keep_attention materialises N x N maps; N <= 8192")
+        maps = []
+        for h in range(hq):
+            s = (Q[h].float() @ K[h // rep].float().T) / d ** 0.5
+            if causal:
+                s = s.masked_fill(torch.ones(n, n, dtype=torch.bool, device=Q.device).triu(1), float("-inf"))
+            maps.append(torch.softmax(s, dim=1))
+    return MultiheadOutput(O, concat_heads(O, output_proj), maps)

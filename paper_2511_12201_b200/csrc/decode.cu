@@ -33,6 +33,17 @@ constexpr int WARP_KEYS = 512;
 constexpr int CTA_KEYS = 4 * WARP_KEYS;
 constexpr int MAXREP = 8;  // rows of the m16 tile used (rows 8..15 stay zero)
 
+// Text / answer segment lengths: one value for the whole batch, or per
+// sequence (serving batches of ragged prompts and answers). The text segment
+// of (sequence s, group g) starts at row (s * Hkv + g) * tcap.
+struct SegLens {
+  const int32_t* tlen;  // nullable: per-sequence text lengths
+  const int32_t* alen;  // nullable: per-sequence answer lengths
+  int nt, na, tcap;
+  __device__ __forceinline__ int text(int s) const { return tlen ? tlen[s] : nt; }
+  __device__ __forceinline__ int answer(int s) const { return alen ? alen[s] : na; }
+};
+
 __device__ __forceinline__ void mma_bf16_16816(float* c, const uint32_t* a, uint32_t b0, uint32_t b1) {
   asm volatile(
       "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
@@ -71,7 +82,7 @@ __global__ void decode_flags_kernel(const __nv_bfloat16* __restrict__ q, const d
 __global__ void __launch_bounds__(128) decode_partial_kernel(
     const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ vk, const __nv_bfloat16* __restrict__ vv,
     const int32_t* __restrict__ vlen, const __nv_bfloat16* __restrict__ tk, const __nv_bfloat16* __restrict__ tv,
-    int nt, const __nv_bfloat16* __restrict__ ak, const __nv_bfloat16* __restrict__ av, int na, int Hq, int Hkv,
+    const __nv_bfloat16* __restrict__ ak, const __nv_bfloat16* __restrict__ av, SegLens sl, int Hq, int Hkv,
     int vcap, int acap, const uint8_t* __restrict__ flags, float* __restrict__ part_ml, float* __restrict__ part_acc,
     int n_chunks) {
   __shared__ float s_ml[4][MAXREP][2];
@@ -86,9 +97,9 @@ __global__ void __launch_bounds__(128) decode_partial_kernel(
   for (int r = 0; r < rep; ++r) any |= flags[(size_t)s * Hq + g * rep + r];
   const bool row_valid = gid < rep;
   const bool row_vis = row_valid && flags[(size_t)s * Hq + g * rep + (row_valid ? gid : 0)];
-  const int vl = vlen[s];
+  const int vl = vlen[s], nt = sl.text(s), tcap = sl.tcap;
   const int k_start = any ? 0 : vl;       // skip the vision segment when every head is lazy
-  const int k_end = vl + nt + na;
+  const int k_end = vl + nt + sl.answer(s);
   const int w0 = k_start + c * CTA_KEYS + warp * WARP_KEYS;
   const int w1 = min(k_end, w0 + WARP_KEYS);
 
@@ -119,14 +130,14 @@ __global__ void __launch_bounds__(128) decode_partial_kernel(
   auto krow = [&](int v) -> const uint4* {
     const __nv_bfloat16* p;
     if (v < vl) p = vk + (sg * vcap + v) * D;
-    else if (v < vl + nt) p = tk + (sg * nt + (v - vl)) * D;
+    else if (v < vl + nt) p = tk + (sg * tcap + (v - vl)) * D;
     else p = ak + (sg * acap + (v - vl - nt)) * D;
     return reinterpret_cast<const uint4*>(p);
   };
   auto vrow = [&](int v) -> const uint4* {
     const __nv_bfloat16* p;
     if (v < vl) p = vv + (sg * vcap + v) * D;
-    else if (v < vl + nt) p = tv + (sg * nt + (v - vl)) * D;
+    else if (v < vl + nt) p = tv + (sg * tcap + (v - vl)) * D;
     else p = av + (sg * acap + (v - vl - nt)) * D;
     return reinterpret_cast<const uint4*>(p);
   };
@@ -312,10 +323,10 @@ __device__ __forceinline__ uint32_t toff(int r, int c) {
 }
 
 struct DecItem {
-  int s, g, c, lo, hi, vl, any;
+  int s, g, c, lo, hi, vl, nt, any;
 };
 
-__device__ __forceinline__ DecItem dec_item(int t, int nc, int Hq, int Hkv, int nt, int na,
+__device__ __forceinline__ DecItem dec_item(int t, int nc, int Hq, int Hkv, const SegLens& sl,
                                             const int32_t* __restrict__ vlen, const uint8_t* __restrict__ flags) {
   DecItem it;
   it.c = t % nc;
@@ -326,15 +337,17 @@ __device__ __forceinline__ DecItem dec_item(int t, int nc, int Hq, int Hkv, int 
   for (int r = 0; r < rep; ++r) any |= flags[(size_t)it.s * Hq + it.g * rep + r];
   it.any = any;
   it.vl = vlen[it.s];
+  it.nt = sl.text(it.s);
   const int k_start = any ? 0 : it.vl;  // skip the vision segment when every head is lazy
-  const int k_end = it.vl + nt + na;
+  const int k_end = it.vl + it.nt + sl.answer(it.s);
   it.lo = k_start + it.c * CTA_KEYS;
   it.hi = min(k_end, it.lo + CTA_KEYS);
   return it;
 }
 
 // tile starting at key k of item `it`: segment, local row, valid keys
-__device__ __forceinline__ void dec_tile(const DecItem& it, int k, int nt, int& seg, int& row, int& nvalid) {
+__device__ __forceinline__ void dec_tile(const DecItem& it, int k, int& seg, int& row, int& nvalid) {
+  const int nt = it.nt;
   int seg_lo, seg_hi;
   if (k < it.vl) { seg = 0; seg_lo = 0; seg_hi = it.vl; }
   else if (k < it.vl + nt) { seg = 1; seg_lo = it.vl; seg_hi = it.vl + nt; }
@@ -347,7 +360,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1) decode_partial_tma_kernel(
     const __grid_constant__ CUtensorMap tm_vk, const __grid_constant__ CUtensorMap tm_vv,
     const __grid_constant__ CUtensorMap tm_tk, const __grid_constant__ CUtensorMap tm_tv,
     const __grid_constant__ CUtensorMap tm_ak, const __grid_constant__ CUtensorMap tm_av,
-    const __nv_bfloat16* __restrict__ q, const int32_t* __restrict__ vlen, int nt, int na, int Hq, int Hkv,
+    const __nv_bfloat16* __restrict__ q, const int32_t* __restrict__ vlen, SegLens sl, int Hq, int Hkv,
     int vcap, int acap, const uint8_t* __restrict__ flags, float* __restrict__ part_ml,
     float* __restrict__ part_acc, int n_chunks, int total_items) {
   extern __shared__ uint8_t dsm_raw[];
@@ -375,11 +388,11 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1) decode_partial_tma_kernel(
       tma_prefetch_desc(&tm_ak); tma_prefetch_desc(&tm_av);
       uint32_t n = 0;
       for (int t = blockIdx.x; t < total_items; t += gridDim.x) {
-        const DecItem it = dec_item(t, n_chunks, Hq, Hkv, nt, na, vlen, flags);
+        const DecItem it = dec_item(t, n_chunks, Hq, Hkv, sl, vlen, flags);
         const int sg = it.s * Hkv + it.g;
         for (int k = it.lo; k < it.hi; k += TK) {
           int seg, row, nv;
-          dec_tile(it, k, nt, seg, row, nv);
+          dec_tile(it, k, seg, row, nv);
           k += nv - TK;  // next tile starts after this tile's valid keys (segment-aligned)
           const int st = n % NSTG;
           if (n >= NSTG) mbar_wait(smem_u32(&empty_bar[st]), ((n / NSTG) - 1) & 1);
@@ -387,7 +400,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1) decode_partial_tma_kernel(
           mbar_expect_tx(fb, TSTAGE);
           const CUtensorMap* mk = seg == 0 ? &tm_vk : seg == 1 ? &tm_tk : &tm_ak;
           const CUtensorMap* mv = seg == 0 ? &tm_vv : seg == 1 ? &tm_tv : &tm_av;
-          const int base = seg == 0 ? sg * vcap : seg == 1 ? sg * nt : sg * acap;
+          const int base = seg == 0 ? sg * vcap : seg == 1 ? sg * sl.tcap : sg * acap;
           const uint32_t kd = sbase + st * TSTAGE, vd = kd + TTILE;
           tma_load_2d(kd, mk, fb, 0, base + row);
           tma_load_2d(kd + TATOM, mk, fb, 64, base + row);
@@ -405,7 +418,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1) decode_partial_tma_kernel(
   const float sl2 = static_cast<float>(kLog2e / sqrt(static_cast<double>(D)));
   uint32_t n = 0;
   for (int t = blockIdx.x; t < total_items; t += gridDim.x) {
-    const DecItem it = dec_item(t, n_chunks, Hq, Hkv, nt, na, vlen, flags);
+    const DecItem it = dec_item(t, n_chunks, Hq, Hkv, sl, vlen, flags);
     const bool row_vis = row_valid && flags[(size_t)it.s * Hq + it.g * rep + (row_valid ? gid : 0)];
     // Q A-fragments, natural head-dim order: k-step ks covers d = 16 ks .. +15
     uint32_t qa[8][4];
@@ -426,7 +439,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1) decode_partial_tma_kernel(
     for (int i = 0; i < 16; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
     for (int k = it.lo; k < it.hi; k += TK) {
       int seg, row, nv;
-      dec_tile(it, k, nt, seg, row, nv);
+      dec_tile(it, k, seg, row, nv);
       const int key0 = k;
       k += nv - TK;
       const int st = n % NSTG;
@@ -552,23 +565,25 @@ extern "C" size_t omni_decode_workspace(int batch, int n_q_heads, int vcap, int 
   return sizeof(float) * (size_t)batch * n_q_heads * nc * (head_dim + 2) + 16;
 }
 
-extern "C" int omni_decode_step(const void* q, const void* vision_k, const void* vision_v, const int32_t* vision_len,
-                                const void* text_k, const void* text_v, int n_text, const void* answer_k,
-                                const void* answer_v, int n_answer, const double* k_lazy, const double* k_act,
-                                int batch, int n_q_heads, int n_kv_heads, int head_dim, int vcap, int acap, double tau,
-                                int preserve_first_head, const uint8_t* flags_override, uint8_t* flags, float* out,
-                                void* workspace, void* stream) {
+static int decode_step_impl(const void* q, const void* vision_k, const void* vision_v, const int32_t* vision_len,
+                            const void* text_k, const void* text_v, const void* answer_k, const void* answer_v,
+                            dec::SegLens sl, const double* k_lazy, const double* k_act, int batch, int n_q_heads,
+                            int n_kv_heads, int head_dim, int vcap, int acap, double tau, int preserve_first_head,
+                            const uint8_t* flags_override, uint8_t* flags, float* out, void* workspace,
+                            int32_t* status, void* stream) {
   OMNI_CHECK(head_dim == dec::D, OMNI_E_SHAPE, "decode kernel requires head_dim == 128");
   OMNI_CHECK(n_kv_heads >= 1 && n_q_heads % n_kv_heads == 0, OMNI_E_SHAPE, "n_q_heads must be a multiple of n_kv_heads");
   OMNI_CHECK(n_q_heads / n_kv_heads <= dec::MAXREP, OMNI_E_SHAPE, "at most 8 Q heads per KV group");
   OMNI_CHECK(tau >= 0.0 && tau < 1.0, OMNI_E_PARAM, "tau must be in [0, 1)");
-  OMNI_CHECK(n_answer >= 0 && n_answer <= acap && n_text >= 0, OMNI_E_SHAPE, "answer segment overflow");
   OMNI_CHECK(batch >= 1, OMNI_E_SHAPE, "empty batch");
+  const int n_text = sl.tcap;
+  const int n_answer = sl.alen ? acap : sl.na;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int nc = dec_chunks(vcap, n_text, n_answer);
   float* part_ml = static_cast<float*>(workspace);
   float* part_acc = part_ml + (size_t)batch * n_q_heads * nc * 2;
-  int* degenerate = reinterpret_cast<int*>(part_acc + (size_t)batch * n_q_heads * nc * head_dim);
+  int* degenerate = status ? reinterpret_cast<int*>(status)
+                           : reinterpret_cast<int*>(part_acc + (size_t)batch * n_q_heads * nc * head_dim);
   OMNI_CUDA_TRY(cudaMemsetAsync(degenerate, 0, sizeof(int), st));
   dec::decode_flags_kernel<<<dim3(n_q_heads, batch), 32, 0, st>>>(static_cast<const __nv_bfloat16*>(q), k_lazy, k_act,
                                                                    n_q_heads, n_kv_heads, tau, preserve_first_head,
@@ -583,8 +598,8 @@ extern "C" int omni_decode_step(const void* q, const void* vision_k, const void*
     dec::decode_partial_kernel<<<dim3(nc, n_kv_heads, batch), 128, 0, st>>>(
         static_cast<const __nv_bfloat16*>(q), static_cast<const __nv_bfloat16*>(vision_k),
         static_cast<const __nv_bfloat16*>(vision_v), vision_len, static_cast<const __nv_bfloat16*>(text_k),
-        static_cast<const __nv_bfloat16*>(text_v), n_text, static_cast<const __nv_bfloat16*>(answer_k),
-        static_cast<const __nv_bfloat16*>(answer_v), n_answer, n_q_heads, n_kv_heads, vcap, acap, flags, part_ml,
+        static_cast<const __nv_bfloat16*>(text_v), static_cast<const __nv_bfloat16*>(answer_k),
+        static_cast<const __nv_bfloat16*>(answer_v), sl, n_q_heads, n_kv_heads, vcap, acap, flags, part_ml,
         part_acc, nc);
   } else {
     CUtensorMap m[6];
@@ -610,13 +625,13 @@ extern "C" int omni_decode_step(const void* q, const void* vision_k, const void*
     OMNI_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     const int items = nc * n_kv_heads * batch;
     dec::decode_partial_tma_kernel<<<min(sms, items), (dec::NCW + 1) * 32, dec::TSMEM, st>>>(
-        m[0], m[1], m[2], m[3], m[4], m[5], static_cast<const __nv_bfloat16*>(q), vision_len, n_text, n_answer,
+        m[0], m[1], m[2], m[3], m[4], m[5], static_cast<const __nv_bfloat16*>(q), vision_len, sl,
         n_q_heads, n_kv_heads, vcap, acap, flags, part_ml, part_acc, nc, items);
   }
   dec::decode_combine_kernel<<<dim3(n_q_heads, batch), dec::D, 0, st>>>(part_ml, part_acc, nc, out, degenerate);
   int st_code = omni_launch_check();
   if (st_code) return st_code;
-  if (n_text + n_answer == 0) {
+  if (!status && n_text + n_answer == 0) {
     // Only reachable degenerate case (decode.py:152-153): read the flag back.
     int h = 0;
     OMNI_CUDA_TRY(cudaMemcpyAsync(&h, degenerate, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -624,4 +639,32 @@ extern "C" int omni_decode_step(const void* q, const void* vision_k, const void*
     OMNI_CHECK(h == 0, OMNI_E_DEGENERATE_CONTEXT, "lazy head with no text and no answer KV");
   }
   return OMNI_OK;
+}
+
+extern "C" int omni_decode_step(const void* q, const void* vision_k, const void* vision_v, const int32_t* vision_len,
+                                const void* text_k, const void* text_v, int n_text, const void* answer_k,
+                                const void* answer_v, int n_answer, const double* k_lazy, const double* k_act,
+                                int batch, int n_q_heads, int n_kv_heads, int head_dim, int vcap, int acap, double tau,
+                                int preserve_first_head, const uint8_t* flags_override, uint8_t* flags, float* out,
+                                void* workspace, void* stream) {
+  OMNI_CHECK(n_answer >= 0 && n_answer <= acap && n_text >= 0, OMNI_E_SHAPE, "answer segment overflow");
+  const dec::SegLens sl{nullptr, nullptr, n_text, n_answer, n_text};
+  return decode_step_impl(q, vision_k, vision_v, vision_len, text_k, text_v, answer_k, answer_v, sl, k_lazy, k_act,
+                          batch, n_q_heads, n_kv_heads, head_dim, vcap, acap, tau, preserve_first_head,
+                          flags_override, flags, out, workspace, nullptr, stream);
+}
+
+extern "C" int omni_decode_step_varlen(const void* q, const void* vision_k, const void* vision_v,
+                                       const int32_t* vision_len, const void* text_k, const void* text_v,
+                                       const int32_t* text_len, int tcap, const void* answer_k, const void* answer_v,
+                                       const int32_t* answer_len, const double* k_lazy, const double* k_act,
+                                       int batch, int n_q_heads, int n_kv_heads, int head_dim, int vcap, int acap,
+                                       double tau, int preserve_first_head, const uint8_t* flags_override,
+                                       uint8_t* flags, float* out, void* workspace, int32_t* status, void* stream) {
+  OMNI_CHECK(text_len && answer_len && status, OMNI_E_PARAM, "varlen decode needs text_len, answer_len and status");
+  OMNI_CHECK(tcap >= 0 && acap >= 0 && tcap + acap > 0, OMNI_E_SHAPE, "text and answer capacities are both zero");
+  const dec::SegLens sl{text_len, answer_len, 0, 0, tcap};
+  return decode_step_impl(q, vision_k, vision_v, vision_len, text_k, text_v, answer_k, answer_v, sl, k_lazy, k_act,
+                          batch, n_q_heads, n_kv_heads, head_dim, vcap, acap, tau, preserve_first_head,
+                          flags_override, flags, out, workspace, status, stream);
 }

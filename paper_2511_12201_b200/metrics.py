@@ -23,6 +23,7 @@ from typing import Any
 import torch
 
 from . import ops
+from .errors import ParameterError
 
 SCHEMA_VERSION = 1
 VALUE_BYTES = 8  # the reference's float64 flat memory model (bytes = values x 8)
@@ -49,6 +50,31 @@ def attention_recall_device(res, Q: torch.Tensor, K: torch.Tensor, V: torch.Tens
     n_act = act.sum(dim=1)
     rec = share.sum(dim=1) / n_act.clamp(min=1).double()
     return torch.where(n_act > 0, rec, torch.ones_like(rec))
+
+
+def sparsity_gap_device(mass: torch.Tensor, selection, n_kv_heads: int, seq_len: int, block_size: int,
+                        p: float) -> float:
+    """kv_select.py:198-210 under rule B: (b_flattest - b_sharpest) / N, each
+    group's individual budget at retention ``p``. The sharpest group is the
+    argmax of the kurtoses K3b already produced (ties to the lowest index, as
+    np.argmax); each budget is K3b run on that group's Q heads alone, so it
+    is the same arithmetic that set the shared budget. ``mass`` is the
+    per-Q-head column mass the selection consumed ([Hq, nb]; nb = N is the
+    exact / token path, block size 1)."""
+    if n_kv_heads < 2:
+        raise ParameterError("sparsity gap needs at least two heads")
+    hq = mass.shape[0]
+    rep = hq // n_kv_heads
+    bs = 1 if mass.shape[1] == seq_len else block_size
+    kurt = selection.stats[:n_kv_heads].cpu().tolist()
+    flat = int(selection.info[1])
+    sharp = max(range(n_kv_heads), key=lambda g: (kurt[g], -g))
+
+    def own_budget(g: int) -> int:
+        sub = mass[g * rep:(g + 1) * rep].contiguous()
+        return int(ops.select(sub, 1, seq_len, bs, p, "token").info[0])
+
+    return (own_budget(flat) - own_budget(sharp)) / seq_len
 
 
 @dataclass(frozen=True)
@@ -194,4 +220,5 @@ def prefill_report(res, Q: torch.Tensor, K: torch.Tensor, V: torch.Tensor, n_vis
         recall_flattest=retained / total if total > 0 else 1.0,
         flattest_retained_mass=retained, flattest_total_mass=total, budget=b, flattest_head=flat,
         lazy_query_fraction=1.0 - float(active[:, :n_vision].float().mean()) if n_vision else 0.0,
-        sparsity_gap=None)
+        sparsity_gap=sparsity_gap_device(res.block_mass, res.selection, hkv, n, cfg.block_size, cfg.p)
+        if hkv >= 2 else None)

@@ -255,5 +255,26 @@ def decode_step(q, vision_k, vision_v, vision_len, text_k, text_v, n_text: int, 
     return out, flags
 
 
+def decode_step_varlen(q, vision_k, vision_v, vision_len, text_k, text_v, text_len, answer_k, answer_v, answer_len,
+                       k_lazy, k_act, tau: float, preserve_first_head: bool, status, flags_override=None, out=None,
+                       flags=None):
+    """K7 over a ragged batch: per-sequence text / answer lengths (device i32
+    [B]); ``status`` (device i32 [1]) receives the degenerate-context flag."""
+    b, hq, d = q.shape
+    hkv, vcap = vision_k.shape[1], vision_k.shape[2]
+    tcap, acap = text_k.shape[2], answer_k.shape[2]
+    dev = q.device
+    if out is None:
+        out = torch.empty(b, hq, d, device=dev, dtype=torch.float32)
+    if flags is None:
+        flags = torch.empty(b, hq, device=dev, dtype=torch.uint8)
+    ws = torch.empty(_lib.size("omni_decode_workspace", b, hq, vcap, tcap, acap, d), device=dev, dtype=torch.uint8)
+    _lib.call("omni_decode_step_varlen", _p(q), _p(vision_k), _p(vision_v), _p(vision_len), _p(text_k), _p(text_v),
+              _p(text_len), tcap, _p(answer_k), _p(answer_v), _p(answer_len), _p(k_lazy), _p(k_act), b, hq, hkv, d,
+              vcap, acap, float(tau), int(bool(preserve_first_head)), _p(flags_override), _p(flags), _p(out), _p(ws),
+              _p(status), _stream())
+    return out, flags
+
+
 def device_check() -> None:
     _lib.call("omni_device_check")

@@ -20,7 +20,7 @@ def dev(x, dtype=torch.bfloat16):
     return torch.tensor(np.asarray(x), dtype=dtype, device="cuda")
 
 
-def build_pair(seed, hq=8, hkv=2, nv=2000, nt=48, steps=6, tau=0.08, lazy=0.5):
+def build_pair(seed, hq=8, hkv=2, nv=2000, nt=48, steps=6, tau=0.08, lazy=0.5, answer_capacity=16):
     from paper_2511_12201_b200 import decode as gdec
     from paper_2511_12201_b200 import ops
     from paper_2511_12201_b200.pipeline import SparsityConfig, sparse_prefill_device
@@ -33,7 +33,7 @@ def build_pair(seed, hq=8, hkv=2, nv=2000, nt=48, steps=6, tau=0.08, lazy=0.5):
     vsel = ops.select(res.block_mass, hkv, n, 256, 0.82, "token", vision_limit=nv, budget_override=b)
     bv = int(vsel.info[0])
     cache = gdec.build_cache(dev(K), dev(V), vsel.selected, bv, nv, nt, res.k_lazy, res.k_act, hq,
-                             answer_capacity=16)
+                             answer_capacity=answer_capacity)
     ref = opipe.select(Q, K, nv, 0, tau, 0.82, 256)
     rb, rsel = opipe.vision_selection(ref, nv)
     assert rb == bv
@@ -107,3 +107,79 @@ def test_batched_decode_ragged_budgets():
         vs = dev(np.stack([p[2][step][2] for p in pairs]))
         gdec.append_answer(batch, ks, vs)
     assert batch.fetch.vision_tokens == sum(l.vision_tokens for l in logs)
+
+
+def test_serving_lifecycle_ragged_admit_evict_grow():
+    """Serving batch: sequences with different vision spans, budgets, prompt
+    text and answer lengths (ragged K7), answer capacity growth, eviction of a
+    finished sequence and admission of a new one mid-stream; every live
+    sequence matches its own oracle at every step."""
+    from paper_2511_12201_b200 import decode as gdec
+
+    specs = [dict(seed=0, nv=2000, nt=48), dict(seed=1, nv=1500, nt=20), dict(seed=2, nv=2300, nt=64)]
+    live = [build_pair(steps=8, answer_capacity=2, **sp) for sp in specs]
+    batch = gdec.stack_caches([p[0] for p in live])
+    assert batch.ragged and batch.text_lens == [48, 20, 64]
+    logs = [oatt.FetchLog() for _ in live]
+    t = [0] * len(live)
+
+    def step():
+        q = np.stack([p[2][t[s]][0] for s, p in enumerate(live)])
+        out, flags = gdec.decode_attention(dev(q), batch, 0.08)
+        for s, (c, oc, tr, rep) in enumerate(live):
+            o_ref, f_ref = oatt.decode_step(tr[t[s]][0], oc, 0.08, rep, True, logs[s])
+            np.testing.assert_array_equal(flags[s].cpu().numpy().astype(bool), f_ref)
+            np.testing.assert_allclose(out[s].cpu().numpy(), np.stack(o_ref), atol=5e-3, rtol=2e-2)
+            oatt.append_answer(oc, tr[t[s]][1], tr[t[s]][2], 128)
+        ks = dev(np.stack([p[2][t[s]][1] for s, p in enumerate(live)]))
+        vs = dev(np.stack([p[2][t[s]][2] for s, p in enumerate(live)]))
+        gdec.append_answer(batch, ks, vs)
+        for s in range(len(live)):
+            t[s] += 1
+
+    for _ in range(3):
+        step()
+    assert batch.answer_k.shape[2] >= 3 and batch.answer_lens == [3, 3, 3]
+    vt = batch.fetch.vision_tokens
+    assert vt == sum(l.vision_tokens for l in logs)
+    # sequence 1 finishes; a new one (different spans) joins with no answer yet
+    batch = gdec.evict(batch, [0, 2])
+    live, logs, t = [live[0], live[2]], [logs[0], logs[2]], [t[0], t[2]]
+    new = build_pair(steps=8, seed=3, nv=1800, nt=33)
+    batch = gdec.admit(batch, new[0])
+    live.append(new)
+    logs.append(oatt.FetchLog())
+    t.append(0)
+    assert batch.answer_lens == [3, 3, 0] and batch.text_lens == [48, 64, 33]
+    for _ in range(3):
+        step()
+    assert batch.answer_lens == [6, 6, 3]
+    # uniform batches stay on the scalar-length kernel; growth past capacity
+    from paper_2511_12201_b200.errors import ShapeError
+
+    u = build_pair(4, answer_capacity=1)[0]
+    z = torch.zeros(1, 2, 128, device="cuda")
+    for _ in range(3):
+        gdec.append_answer(u, z, z)
+    assert not u.ragged and u.n_answer == 3 and u.answer_k.shape[2] >= 3
+    while u.n_answer < u.answer_k.shape[2]:
+        gdec.append_answer(u, z, z)
+    with pytest.raises(ShapeError):
+        gdec.append_answer(u, z, z, grow=False)
+
+
+def test_ragged_degenerate_context_flag():
+    """A ragged batch member with no text and no answer rows and a lazy head
+    raises DegenerateContextError (decode.py:152-153) via the device status."""
+    from paper_2511_12201_b200 import decode as gdec
+    from paper_2511_12201_b200.errors import DegenerateContextError
+
+    a = build_pair(0)[0]
+    b, _, trace, _ = build_pair(1, nt=0, lazy=0.9)
+    batch = gdec.stack_caches([a, b])
+    assert batch.ragged and batch.text_lens == [48, 0]
+    q = np.stack([trace[0][0], trace[0][0]])
+    forced = np.ones((2, 8), dtype=bool)
+    forced[1, 3] = False  # a lazy head of the context-less sequence
+    with pytest.raises(DegenerateContextError):
+        gdec.decode_attention(dev(q), batch, 0.08, flags=torch.tensor(forced))

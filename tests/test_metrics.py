@@ -139,3 +139,32 @@ def test_cli_modes_and_determinism(tmp_path):
     assert len(sweep) == 4
     dec = gm.MetricsReport.from_json(_cli(["--mode", "decode", "--steps", "4", *common], tmp_path, "d.json"))
     assert dec.decode["vision_tokens_fetched"] == dec.decode["predicted_vision_tokens"]  # AC6 exactness
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("source", ["probe", "exact"])
+def test_gpu_sparsity_gap_matches_oracle(source):
+    """kv_select.py:198-210 under rule B: the flattest and sharpest groups'
+    individual budgets (K3b on each group alone) vs the oracle's budgets on
+    the same group score vectors (bit-exact). The SPEC.md:596 trend is a
+    statistical property over many synthetic trials, not asserted here."""
+    import torch
+
+    from oracle import pipeline as opipe
+    from oracle import selection as osel
+    from oracle.workload import Spec, generate, round_bf16
+    from paper_2511_12201_b200.pipeline import SparsityConfig, select_device
+
+    Q, K, V = generate(Spec(heads=8, heads_kv=4, head_dim=128, n_vision=3000, n_text=72, seed=5))
+    Q, K = round_bf16(Q), round_bf16(K)
+    t = lambda x: torch.tensor(x, dtype=torch.bfloat16, device="cuda")
+    Qd, Kd = t(Q), t(K)
+    n = Q.shape[1]
+    for p in (0.2, 0.82):
+        cfg = SparsityConfig(p=p)
+        *_, mass, sel = select_device(Qd, Kd, 3000, cfg, score_source=source)
+        ref = opipe.select(Q, K, 3000, 0, cfg.tau, p, 256, score_source=source)
+        assert int(sel.info[0]) == ref.budget
+        got = gm.sparsity_gap_device(mass, sel, 4, n, cfg.block_size, p)
+        exp = osel.sparsity_gap(ref.group_scores, p)
+        assert got == exp, (p, got, exp)
