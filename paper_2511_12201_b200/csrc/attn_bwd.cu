@@ -27,6 +27,19 @@ namespace omni {
 namespace bwd {
 
 constexpr int D = 128;
+// Exponential pairs (of 16 per 32-column chunk) evaluated by the FMA-pipe
+// polynomial instead of MUFU.EX2 in the dS math of dq / dkv (the MUFU is the
+// co-bottleneck there as in K4); masked entries are discarded by a select,
+// so the polynomial's behaviour on them does not matter.
+#ifndef OMNI_BWD_POLY
+#define OMNI_BWD_POLY 0
+#endif
+__device__ __forceinline__ constexpr bool bwd_poly(int pair) {
+  return OMNI_BWD_POLY > 0 && ((pair * OMNI_BWD_POLY) % 16) < OMNI_BWD_POLY;
+}
+__device__ __forceinline__ uint64_t exp2_pair(uint64_t x, bool poly, const Exp2PolyConsts& pc) {
+  return poly ? exp2_poly_pair(x, pc) : f32x2(fast_exp2(f32x2_lo(x)), fast_exp2(f32x2_hi(x)));
+}
 constexpr uint32_t ATOM = 128 * 128;  // 128 rows x 128 B swizzle region
 constexpr uint32_t TILE = 2 * ATOM;   // 128 x 128 bf16
 
@@ -234,6 +247,8 @@ dq_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
     const float Dv = valid ? __ldg(Dc + ci) : 0.f;
     const uint32_t tl = tmem + ((uint32_t)((warp & 3) * 32) << 16);
     const float sl2 = static_cast<float>(kLog2e / sqrt(static_cast<double>(D)));
+    const uint64_t c2 = f32x2(sl2, sl2), nl2 = f32x2(-l2, -l2), nD2 = f32x2(-Dv, -Dv);
+    const Exp2PolyConsts pc = exp2_poly_consts();
     uint8_t* ds_gen = smem + OFF_DS;
     for (int j = 0; j < nt; ++j) {
       mbar_wait(B(B_SF), j & 1);
@@ -246,13 +261,21 @@ dq_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
       tc_fence_before();
       mbar_arrive(B(B_SE));  // S / dP of this tile consumed: the next tile's MMAs may overwrite them
       const int lim = vis - j * 128;
+      // paired FP32 ops: x = s log2e/sqrt(d) - lse2, dS = 2^x (dP - D); the
+      // visibility compare only on staircase tiles
+      const bool full = __all_sync(0xffffffffu, lim >= cb + 32);
       uint32_t pk[16];
 #pragma unroll
       for (int c = 0; c < 32; c += 2) {
-        const int col = cb + c;
-        const float p0 = (col < lim) ? fast_exp2(__uint_as_float(s[c]) * sl2 - l2) : 0.f;
-        const float p1 = (col + 1 < lim) ? fast_exp2(__uint_as_float(s[c + 1]) * sl2 - l2) : 0.f;
-        pk[c / 2] = pack_bf16x2(p0 * (__uint_as_float(p[c]) - Dv), p1 * (__uint_as_float(p[c + 1]) - Dv));
+        const uint64_t xl = ffma2(f32x2(__uint_as_float(s[c]), __uint_as_float(s[c + 1])), c2, nl2);
+        const uint64_t ex = exp2_pair(xl, bwd_poly(c >> 1), pc);
+        float p0 = f32x2_lo(ex), p1 = f32x2_hi(ex);
+        if (!full) {
+          p0 = (cb + c < lim) ? p0 : 0.f;
+          p1 = (cb + c + 1 < lim) ? p1 : 0.f;
+        }
+        const uint64_t ds = fmul2(f32x2(p0, p1), fadd2(f32x2(__uint_as_float(p[c]), __uint_as_float(p[c + 1])), nD2));
+        pk[c / 2] = pack_bf16x2(f32x2_lo(ds), f32x2_hi(ds));
       }
       if (j > 0) mbar_wait(B(B_DSE), (j - 1) & 1);  // dQ MMA of j-1 finished reading dS
 #pragma unroll
@@ -586,6 +609,10 @@ constexpr uint32_t COL_S = 0, COL_DP = 128, COL_DV = 256, COL_DK = 384;
 constexpr int NTHREADS = 640;  // TMA, MMA, 2 row-info warps, 16 gradient warps
 }  // namespace dkv2
 
+// PROBE (profiling only, OMNI_BWD_PROBE): 1 = gradient warps release P^T /
+// dS^T without computing them (the MMA / TMA pipeline floor); 2 = the
+// gradient arithmetic without the exponentials (MUFU share).
+template <int PROBE>
 __global__ void __launch_bounds__(dkv2::NTHREADS, 1)
 dkv2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
             const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
@@ -729,8 +756,8 @@ dkv2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
       if (k >= 2) mbar_wait(B(B_IE + s), ((k >> 1) - 1) & 1);
       for (int rr = r; rr < BR; rr += 64) {
         const size_t ci = (size_t)h * capq + (first + k) * BR + rr;
-        info[(s * 3 + 0) * BR + rr] = __ldg(lse2c + ci);
-        info[(s * 3 + 1) * BR + rr] = __ldg(Dc + ci);
+        info[(s * 3 + 0) * BR + rr] = -__ldg(lse2c + ci);  // negated: one FFMA2 / FADD2 per pair
+        info[(s * 3 + 1) * BR + rr] = -__ldg(Dc + ci);
         reinterpret_cast<int*>(info)[(s * 3 + 2) * BR + rr] = __ldg(visc + ci);
       }
       mbar_arrive(B(B_IF + s));
@@ -756,17 +783,51 @@ dkv2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
       tmem_wait_ld();
       tc_fence_before();
       mbar_arrive(B(B_SE));
+      if constexpr (PROBE == 1) {
+        mbar_wait(B(B_IF + s), (k >> 1) & 1);
+        mbar_arrive(B(B_IE + s));
+        mbar_arrive(B(B_PF));
+        continue;
+      }
       mbar_wait(B(B_IF + s), (k >> 1) & 1);
-      const float* l2 = info + (s * 3 + 0) * BR + cb;
-      const float* dd = info + (s * 3 + 1) * BR + cb;
-      const int* vv = reinterpret_cast<const int*>(info) + (s * 3 + 2) * BR + cb;
+      // pairs of rows on the paired FP32 pipe: x = s log2e/sqrt(d) - lse2,
+      // P = 2^x (0 beyond a row's visible keys), dS = P (dP - D)
+      const uint32_t a_l2 = smem_u32(info + (s * 3 + 0) * BR + cb), a_dd = smem_u32(info + (s * 3 + 1) * BR + cb);
+      const uint32_t a_vv = smem_u32(info + (s * 3 + 2) * BR + cb);
+      // rows ascend, so do their visible-key counts: every one of this
+      // thread's 32 rows sees key kj iff the first one does
+      const bool full = __all_sync(0xffffffffu, kj < lds_i4(a_vv).x);
+      const uint64_t c2 = f32x2(sl2, sl2);
+      const Exp2PolyConsts pc = exp2_poly_consts();
       uint32_t pp[16], pd[16];
 #pragma unroll
-      for (int c = 0; c < 32; c += 2) {
-        const float p0 = (kj < vv[c]) ? fast_exp2(__uint_as_float(sv[c]) * sl2 - l2[c]) : 0.f;
-        const float p1 = (kj < vv[c + 1]) ? fast_exp2(__uint_as_float(sv[c + 1]) * sl2 - l2[c + 1]) : 0.f;
-        pp[c / 2] = pack_bf16x2(p0, p1);
-        pd[c / 2] = pack_bf16x2(p0 * (__uint_as_float(dp[c]) - dd[c]), p1 * (__uint_as_float(dp[c + 1]) - dd[c + 1]));
+      for (int c4 = 0; c4 < 8; ++c4) {
+        const float4 L = lds_f4(a_l2 + 16 * c4), Dn = lds_f4(a_dd + 16 * c4);
+        int4 Vi = make_int4(0, 0, 0, 0);
+        if (!full) Vi = lds_i4(a_vv + 16 * c4);
+#pragma unroll
+        for (int hp = 0; hp < 2; ++hp) {
+          const int c = 4 * c4 + 2 * hp;
+          const uint64_t xl = ffma2(f32x2(__uint_as_float(sv[c]), __uint_as_float(sv[c + 1])), c2,
+                                    hp ? f32x2(L.z, L.w) : f32x2(L.x, L.y));
+          float p0, p1;
+          if constexpr (PROBE == 2) {
+            p0 = f32x2_lo(xl);
+            p1 = f32x2_hi(xl);
+          } else {
+            const uint64_t ex = exp2_pair(xl, bwd_poly(c >> 1), pc);
+            p0 = f32x2_lo(ex);
+            p1 = f32x2_hi(ex);
+          }
+          if (!full) {
+            p0 = kj < (hp ? Vi.z : Vi.x) ? p0 : 0.f;
+            p1 = kj < (hp ? Vi.w : Vi.y) ? p1 : 0.f;
+          }
+          const uint64_t ds = fmul2(f32x2(p0, p1), fadd2(f32x2(__uint_as_float(dp[c]), __uint_as_float(dp[c + 1])),
+                                                           hp ? f32x2(Dn.z, Dn.w) : f32x2(Dn.x, Dn.y)));
+          pp[c / 2] = pack_bf16x2(p0, p1);
+          pd[c / 2] = pack_bf16x2(f32x2_lo(ds), f32x2_hi(ds));
+        }
       }
       mbar_arrive(B(B_IE + s));
       // P^T / dS^T over this thread's own (already read) dP^T columns; dV / dK(k-1)
@@ -884,13 +945,17 @@ extern "C" int omni_sparse_attn_bwd(const void* Q, const void* K_sel, const void
         tq64, tdo64, tk, tv, rows, counts, selected, sel_counts, lse2c, Dc, visc, rep, seq_len, cap, capq, dK_sel,
         dV_sel);
   } else {
+    static const int probe = [] {
+      const char* e = getenv("OMNI_BWD_PROBE");
+      return e ? atoi(e) : 0;
+    }();
+    auto kern = probe == 1 ? bwd::dkv2_kernel<1> : probe == 2 ? bwd::dkv2_kernel<2> : bwd::dkv2_kernel<0>;
     static bool attr2 = false;
     if (!attr2) {
-      OMNI_CUDA_TRY(cudaFuncSetAttribute(bwd::dkv2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)bwd::dkv2::SMEM));
+      OMNI_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bwd::dkv2::SMEM));
       attr2 = true;
     }
-    bwd::dkv2_kernel<<<dim3(cap / 128, n_kv_heads * rep), bwd::dkv2::NTHREADS, bwd::dkv2::SMEM, st>>>(
+    kern<<<dim3(cap / 128, n_kv_heads * rep), bwd::dkv2::NTHREADS, bwd::dkv2::SMEM, st>>>(
         tq128, tdo128, tk, tv, rows, counts, selected, sel_counts, lse2c, Dc, visc, rep, seq_len, cap, capq, dK_sel,
         dV_sel);
   }
