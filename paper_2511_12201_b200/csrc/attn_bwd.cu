@@ -248,7 +248,6 @@ dq_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
     const uint32_t tl = tmem + ((uint32_t)((warp & 3) * 32) << 16);
     const float sl2 = static_cast<float>(kLog2e / sqrt(static_cast<double>(D)));
     const uint64_t c2 = f32x2(sl2, sl2), nl2 = f32x2(-l2, -l2), nD2 = f32x2(-Dv, -Dv);
-    const Exp2PolyConsts pc = exp2_poly_consts();
     uint8_t* ds_gen = smem + OFF_DS;
     for (int j = 0; j < nt; ++j) {
       mbar_wait(B(B_SF), j & 1);
@@ -265,18 +264,22 @@ dq_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
       // visibility compare only on staircase tiles
       const bool full = __all_sync(0xffffffffu, lim >= cb + 32);
       uint32_t pk[16];
+      auto math = [&](auto full_c) {  // separate full / staircase code (issue-bound loop)
+        constexpr bool FULL = decltype(full_c)::value;
 #pragma unroll
-      for (int c = 0; c < 32; c += 2) {
-        const uint64_t xl = ffma2(f32x2(__uint_as_float(s[c]), __uint_as_float(s[c + 1])), c2, nl2);
-        const uint64_t ex = exp2_pair(xl, bwd_poly(c >> 1), pc);
-        float p0 = f32x2_lo(ex), p1 = f32x2_hi(ex);
-        if (!full) {
-          p0 = (cb + c < lim) ? p0 : 0.f;
-          p1 = (cb + c + 1 < lim) ? p1 : 0.f;
+        for (int c = 0; c < 32; c += 2) {
+          const uint64_t xl = ffma2(f32x2(__uint_as_float(s[c]), __uint_as_float(s[c + 1])), c2, nl2);
+          float p0 = fast_exp2(f32x2_lo(xl)), p1 = fast_exp2(f32x2_hi(xl));
+          if constexpr (!FULL) {
+            p0 = (cb + c < lim) ? p0 : 0.f;
+            p1 = (cb + c + 1 < lim) ? p1 : 0.f;
+          }
+          const uint64_t ds =
+              fmul2(f32x2(p0, p1), fadd2(f32x2(__uint_as_float(p[c]), __uint_as_float(p[c + 1])), nD2));
+          pk[c / 2] = pack_bf16x2(f32x2_lo(ds), f32x2_hi(ds));
         }
-        const uint64_t ds = fmul2(f32x2(p0, p1), fadd2(f32x2(__uint_as_float(p[c]), __uint_as_float(p[c + 1])), nD2));
-        pk[c / 2] = pack_bf16x2(f32x2_lo(ds), f32x2_hi(ds));
-      }
+      };
+      if (full) math(std::true_type{}); else math(std::false_type{});
       if (j > 0) mbar_wait(B(B_DSE), (j - 1) & 1);  // dQ MMA of j-1 finished reading dS
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
@@ -600,9 +603,10 @@ dkv_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUt
 namespace dkv2 {
 constexpr int BR = 128;
 constexpr uint32_t OFF_K = 0, OFF_V = TILE, OFF_Q = 2 * TILE, OFF_DO = 4 * TILE;  // Q, dO: 2 stages each
-constexpr uint32_t OFF_INFO = 6 * TILE;                                           // [2][3][128]
-constexpr uint32_t OFF_BAR = OFF_INFO + 2 * 3 * BR * 4;
-enum { B_KV = 0, B_QF = 1, B_QE = 3, B_IF = 5, B_IE = 7, B_SF = 9, B_SE = 10, B_PF = 11, B_PE = 12, B_N = 13 };
+constexpr int NI = 4;                                                             // row-info ring depth
+constexpr uint32_t OFF_INFO = 6 * TILE;                                           // [NI][3][128]
+constexpr uint32_t OFF_BAR = OFF_INFO + NI * 3 * BR * 4;
+enum { B_KV = 0, B_QF = 1, B_QE = 3, B_IF = 5, B_IE = 5 + NI, B_SF = 5 + 2 * NI, B_SE, B_PF, B_PE, B_N };
 constexpr uint32_t OFF_TMEM = OFF_BAR + 8 * B_N;
 constexpr uint32_t SMEM = OFF_TMEM + 16 + 1024;
 constexpr uint32_t COL_S = 0, COL_DP = 128, COL_DV = 256, COL_DK = 384;
@@ -611,7 +615,10 @@ constexpr int NTHREADS = 640;  // TMA, MMA, 2 row-info warps, 16 gradient warps
 
 // PROBE (profiling only, OMNI_BWD_PROBE): 1 = gradient warps release P^T /
 // dS^T without computing them (the MMA / TMA pipeline floor); 2 = the
-// gradient arithmetic without the exponentials (MUFU share).
+// gradient arithmetic without the exponentials (MUFU share); 3 = per-phase
+// cycle sums (lane 0 of each gradient warp and of the MMA warp) into
+// g_bwd_trace, read back with omni_debug_bwd_trace.
+__device__ unsigned long long g_bwd_trace[8];
 template <int PROBE>
 __global__ void __launch_bounds__(dkv2::NTHREADS, 1)
 dkv2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
@@ -655,6 +662,8 @@ dkv2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
     for (int s = 0; s < 2; ++s) {
       mbar_init(B(B_QF + s), 1);
       mbar_init(B(B_QE + s), 1);
+    }
+    for (int s = 0; s < NI; ++s) {
       mbar_init(B(B_IF + s), 64);
       mbar_init(B(B_IE + s), 512);
     }
@@ -723,12 +732,20 @@ dkv2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
       mbar_wait(B(B_KV), 0);
       issue_st(0);
       issue_dpt(0);
+      uint32_t tw_se = 0, tw_pf = 0;
       for (int k = 0; k < total; ++k) {
         const int s = k & 1;
+        const uint32_t t0 = clock();
         mbar_wait(B(B_SE), k & 1);  // S^T(k), dP^T(k) read by every gradient thread
         tc_fence_after();
+        const uint32_t t1 = clock();
         if (k + 1 < total) issue_st(k + 1);
+        const uint32_t t2 = clock();
         mbar_wait(B(B_PF), k & 1);  // P^T(k), dS^T(k) in TMEM
+        if constexpr (PROBE == 3) {
+          tw_se += t1 - t0;
+          tw_pf += clock() - t2;
+        }
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {  // K = 128 rows, 16 per MMA
@@ -746,14 +763,21 @@ dkv2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
         umma_commit_ws(B(B_PE));
         if (k + 1 < total) issue_dpt(k + 1);  // after dV / dK(k): they read the dP^T region
       }
+      if constexpr (PROBE == 3) {
+        if (lane == 0) {
+          atomicAdd(&g_bwd_trace[4], (unsigned long long)tw_se);
+          (void)tw_pf;
+          atomicAdd(&g_bwd_trace[7], (unsigned long long)total);
+        }
+      }
     }
   } else if (warp == 2 || warp == 3) {
     // row-info loader: lse2 / D / vis of the 128 rows of each Q tile -> smem ring
     const int r = threadIdx.x - 64;  // rows r and r + 64
     float* info = reinterpret_cast<float*>(smem + OFF_INFO);
     for (int k = 0; k < total; ++k) {
-      const int s = k & 1;
-      if (k >= 2) mbar_wait(B(B_IE + s), ((k >> 1) - 1) & 1);
+      const int s = k % NI;  // loaded NI - 1 Q tiles ahead of its use (global latency)
+      if (k >= NI) mbar_wait(B(B_IE + s), ((k / NI) - 1) & 1);
       for (int rr = r; rr < BR; rr += 64) {
         const size_t ci = (size_t)h * capq + (first + k) * BR + rr;
         info[(s * 3 + 0) * BR + rr] = -__ldg(lse2c + ci);  // negated: one FFMA2 / FADD2 per pair
@@ -772,64 +796,72 @@ dkv2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
     const float sl2 = static_cast<float>(kLog2e / sqrt(static_cast<double>(D)));
     const float* info = reinterpret_cast<const float*>(smem + OFF_INFO);
     const int cb = cq * 32;
+    uint32_t tg[5] = {0, 0, 0, 0, 0};
     for (int k = 0; k < total; ++k) {
-      const int s = k & 1;
+      const uint32_t c0 = clock();
       mbar_wait(B(B_SF), k & 1);
       tc_fence_after();
+      const uint32_t c1 = clock();
       uint32_t sv[32], dp[32];
       __syncwarp();
       tmem_ld32(tl + COL_S + cb, sv);
       tmem_ld32(tl + COL_DP + cb, dp);
       tmem_wait_ld();
+      const uint32_t c2c = clock();
       tc_fence_before();
       mbar_arrive(B(B_SE));
       if constexpr (PROBE == 1) {
-        mbar_wait(B(B_IF + s), (k >> 1) & 1);
-        mbar_arrive(B(B_IE + s));
+        mbar_wait(B(B_IF + k % NI), (k / NI) & 1);
+        mbar_arrive(B(B_IE + k % NI));
         mbar_arrive(B(B_PF));
         continue;
       }
-      mbar_wait(B(B_IF + s), (k >> 1) & 1);
+      const int si = k % NI;
+      mbar_wait(B(B_IF + si), (k / NI) & 1);
+      const uint32_t c2i = clock();
+      if constexpr (PROBE == 3) tg[4] += c2i - c2c;
       // pairs of rows on the paired FP32 pipe: x = s log2e/sqrt(d) - lse2,
       // P = 2^x (0 beyond a row's visible keys), dS = P (dP - D)
-      const uint32_t a_l2 = smem_u32(info + (s * 3 + 0) * BR + cb), a_dd = smem_u32(info + (s * 3 + 1) * BR + cb);
-      const uint32_t a_vv = smem_u32(info + (s * 3 + 2) * BR + cb);
+      const uint32_t a_l2 = smem_u32(info + (si * 3 + 0) * BR + cb), a_dd = smem_u32(info + (si * 3 + 1) * BR + cb);
+      const uint32_t a_vv = smem_u32(info + (si * 3 + 2) * BR + cb);
       // rows ascend, so do their visible-key counts: every one of this
       // thread's 32 rows sees key kj iff the first one does
       const bool full = __all_sync(0xffffffffu, kj < lds_i4(a_vv).x);
       const uint64_t c2 = f32x2(sl2, sl2);
-      const Exp2PolyConsts pc = exp2_poly_consts();
       uint32_t pp[16], pd[16];
+      // separate instantiations for full and staircase tiles: predicated-off
+      // selects would still take issue slots (the loop is issue-bound)
+      auto math = [&](auto full_c) {
+        constexpr bool FULL = decltype(full_c)::value;
 #pragma unroll
-      for (int c4 = 0; c4 < 8; ++c4) {
-        const float4 L = lds_f4(a_l2 + 16 * c4), Dn = lds_f4(a_dd + 16 * c4);
-        int4 Vi = make_int4(0, 0, 0, 0);
-        if (!full) Vi = lds_i4(a_vv + 16 * c4);
+        for (int c4 = 0; c4 < 8; ++c4) {
+          const float4 L = lds_f4(a_l2 + 16 * c4), Dn = lds_f4(a_dd + 16 * c4);
+          int4 Vi;
+          if constexpr (!FULL) Vi = lds_i4(a_vv + 16 * c4);
 #pragma unroll
-        for (int hp = 0; hp < 2; ++hp) {
-          const int c = 4 * c4 + 2 * hp;
-          const uint64_t xl = ffma2(f32x2(__uint_as_float(sv[c]), __uint_as_float(sv[c + 1])), c2,
-                                    hp ? f32x2(L.z, L.w) : f32x2(L.x, L.y));
-          float p0, p1;
-          if constexpr (PROBE == 2) {
-            p0 = f32x2_lo(xl);
-            p1 = f32x2_hi(xl);
-          } else {
-            const uint64_t ex = exp2_pair(xl, bwd_poly(c >> 1), pc);
-            p0 = f32x2_lo(ex);
-            p1 = f32x2_hi(ex);
+          for (int hp = 0; hp < 2; ++hp) {
+            const int c = 4 * c4 + 2 * hp;
+            const uint64_t xl = ffma2(f32x2(__uint_as_float(sv[c]), __uint_as_float(sv[c + 1])), c2,
+                                      hp ? f32x2(L.z, L.w) : f32x2(L.x, L.y));
+            float p0 = f32x2_lo(xl), p1 = f32x2_hi(xl);
+            if constexpr (PROBE != 2) {
+              p0 = fast_exp2(p0);
+              p1 = fast_exp2(p1);
+            }
+            if constexpr (!FULL) {
+              p0 = kj < (hp ? Vi.z : Vi.x) ? p0 : 0.f;
+              p1 = kj < (hp ? Vi.w : Vi.y) ? p1 : 0.f;
+            }
+            const uint64_t ds = fmul2(f32x2(p0, p1), fadd2(f32x2(__uint_as_float(dp[c]), __uint_as_float(dp[c + 1])),
+                                                             hp ? f32x2(Dn.z, Dn.w) : f32x2(Dn.x, Dn.y)));
+            pp[c / 2] = pack_bf16x2(p0, p1);
+            pd[c / 2] = pack_bf16x2(f32x2_lo(ds), f32x2_hi(ds));
           }
-          if (!full) {
-            p0 = kj < (hp ? Vi.z : Vi.x) ? p0 : 0.f;
-            p1 = kj < (hp ? Vi.w : Vi.y) ? p1 : 0.f;
-          }
-          const uint64_t ds = fmul2(f32x2(p0, p1), fadd2(f32x2(__uint_as_float(dp[c]), __uint_as_float(dp[c + 1])),
-                                                           hp ? f32x2(Dn.z, Dn.w) : f32x2(Dn.x, Dn.y)));
-          pp[c / 2] = pack_bf16x2(p0, p1);
-          pd[c / 2] = pack_bf16x2(f32x2_lo(ds), f32x2_hi(ds));
         }
-      }
-      mbar_arrive(B(B_IE + s));
+      };
+      if (full) math(std::true_type{}); else math(std::false_type{});
+      mbar_arrive(B(B_IE + si));
+      const uint32_t c3 = clock();
       // P^T / dS^T over this thread's own (already read) dP^T columns; dV / dK(k-1)
       // finished reading the region before dP^T(k) was computed (in-order tensor pipe)
       __syncwarp();
@@ -838,6 +870,20 @@ dkv2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
       tmem_wait_st();
       tc_fence_before();
       mbar_arrive(B(B_PF));
+      if constexpr (PROBE == 3) {
+        const uint32_t c4 = clock();
+        tg[0] += c1 - c0;
+        tg[1] += c2c - c1;
+        tg[2] += c3 - c2i;
+        tg[3] += c4 - c3;
+      }
+    }
+    if constexpr (PROBE == 3) {
+      if (lane == 0) {
+        for (int q = 0; q < 4; ++q) atomicAdd(&g_bwd_trace[q], (unsigned long long)tg[q]);
+        atomicAdd(&g_bwd_trace[6], (unsigned long long)total);
+        atomicAdd(&g_bwd_trace[5], (unsigned long long)tg[4]);  // (overrides the MMA PF wait slot)
+      }
     }
     const bool valid = kj < nsel;
     const int dcb = cq * 32;  // this thread's 32 head-dim columns of dK / dV
@@ -949,7 +995,10 @@ extern "C" int omni_sparse_attn_bwd(const void* Q, const void* K_sel, const void
       const char* e = getenv("OMNI_BWD_PROBE");
       return e ? atoi(e) : 0;
     }();
-    auto kern = probe == 1 ? bwd::dkv2_kernel<1> : probe == 2 ? bwd::dkv2_kernel<2> : bwd::dkv2_kernel<0>;
+    auto kern = probe == 1   ? bwd::dkv2_kernel<1>
+                : probe == 2 ? bwd::dkv2_kernel<2>
+                : probe == 3 ? bwd::dkv2_kernel<3>
+                             : bwd::dkv2_kernel<0>;
     static bool attr2 = false;
     if (!attr2) {
       OMNI_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bwd::dkv2::SMEM));
@@ -960,4 +1009,13 @@ extern "C" int omni_sparse_attn_bwd(const void* Q, const void* K_sel, const void
         dV_sel);
   }
   return omni_launch_check();
+}
+
+// Profiling support (OMNI_BWD_PROBE=3): copies the 8 dkv phase-cycle sums to
+// host memory and resets them.
+extern "C" int omni_debug_bwd_trace(unsigned long long* host8) {
+  OMNI_CUDA_TRY(cudaMemcpyFromSymbol(host8, bwd::g_bwd_trace, sizeof(unsigned long long) * 8));
+  unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  OMNI_CUDA_TRY(cudaMemcpyToSymbol(bwd::g_bwd_trace, z, sizeof(z)));
+  return OMNI_OK;
 }
