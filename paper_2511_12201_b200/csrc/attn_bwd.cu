@@ -28,17 +28,21 @@ namespace bwd {
 
 constexpr int D = 128;
 // Exponential pairs (of 16 per 32-column chunk) evaluated by the FMA-pipe
-// polynomial instead of MUFU.EX2 in the dS math of dq / dkv (the MUFU is the
-// co-bottleneck there as in K4); masked entries are discarded by a select,
-// so the polynomial's behaviour on them does not matter.
+// polynomial instead of MUFU.EX2 in the dS math of dkv / dq (the MUFU is the
+// co-bottleneck there as in K4; measured at C4: 4 of 16 is best for both,
+// dkv 5.16 -> 4.68 ms); masked entries are discarded by a select, so the
+// polynomial's behaviour on them does not matter.
 #ifndef OMNI_BWD_POLY
-#define OMNI_BWD_POLY 0
+#define OMNI_BWD_POLY 4
+#endif
+#ifndef OMNI_DQ_POLY
+#define OMNI_DQ_POLY 4
 #endif
 __device__ __forceinline__ constexpr bool bwd_poly(int pair) {
   return OMNI_BWD_POLY > 0 && ((pair * OMNI_BWD_POLY) % 16) < OMNI_BWD_POLY;
 }
-__device__ __forceinline__ uint64_t exp2_pair(uint64_t x, bool poly, const Exp2PolyConsts& pc) {
-  return poly ? exp2_poly_pair(x, pc) : f32x2(fast_exp2(f32x2_lo(x)), fast_exp2(f32x2_hi(x)));
+__device__ __forceinline__ constexpr bool dq_poly(int pair) {
+  return OMNI_DQ_POLY > 0 && ((pair * OMNI_DQ_POLY) % 16) < OMNI_DQ_POLY;
 }
 constexpr uint32_t ATOM = 128 * 128;  // 128 rows x 128 B swizzle region
 constexpr uint32_t TILE = 2 * ATOM;   // 128 x 128 bf16
@@ -248,6 +252,7 @@ dq_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
     const uint32_t tl = tmem + ((uint32_t)((warp & 3) * 32) << 16);
     const float sl2 = static_cast<float>(kLog2e / sqrt(static_cast<double>(D)));
     const uint64_t c2 = f32x2(sl2, sl2), nl2 = f32x2(-l2, -l2), nD2 = f32x2(-Dv, -Dv);
+    const Exp2PolyConsts pc = exp2_poly_consts();
     uint8_t* ds_gen = smem + OFF_DS;
     for (int j = 0; j < nt; ++j) {
       mbar_wait(B(B_SF), j & 1);
@@ -269,7 +274,15 @@ dq_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
 #pragma unroll
         for (int c = 0; c < 32; c += 2) {
           const uint64_t xl = ffma2(f32x2(__uint_as_float(s[c]), __uint_as_float(s[c + 1])), c2, nl2);
-          float p0 = fast_exp2(f32x2_lo(xl)), p1 = fast_exp2(f32x2_hi(xl));
+          float p0, p1;
+          if (dq_poly(c >> 1)) {
+            const uint64_t ex = exp2_poly_pair(xl, pc);
+            p0 = f32x2_lo(ex);
+            p1 = f32x2_hi(ex);
+          } else {
+            p0 = fast_exp2(f32x2_lo(xl));
+            p1 = fast_exp2(f32x2_hi(xl));
+          }
           if constexpr (!FULL) {
             p0 = (cb + c < lim) ? p0 : 0.f;
             p1 = (cb + c + 1 < lim) ? p1 : 0.f;
@@ -828,6 +841,7 @@ dkv2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
       // thread's 32 rows sees key kj iff the first one does
       const bool full = __all_sync(0xffffffffu, kj < lds_i4(a_vv).x);
       const uint64_t c2 = f32x2(sl2, sl2);
+      const Exp2PolyConsts pc = exp2_poly_consts();
       uint32_t pp[16], pd[16];
       // separate instantiations for full and staircase tiles: predicated-off
       // selects would still take issue slots (the loop is issue-bound)
@@ -845,8 +859,14 @@ dkv2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
                                       hp ? f32x2(L.z, L.w) : f32x2(L.x, L.y));
             float p0 = f32x2_lo(xl), p1 = f32x2_hi(xl);
             if constexpr (PROBE != 2) {
-              p0 = fast_exp2(p0);
-              p1 = fast_exp2(p1);
+              if (bwd_poly(c >> 1)) {
+                const uint64_t ex = exp2_poly_pair(xl, pc);
+                p0 = f32x2_lo(ex);
+                p1 = f32x2_hi(ex);
+              } else {
+                p0 = fast_exp2(p0);
+                p1 = fast_exp2(p1);
+              }
             }
             if constexpr (!FULL) {
               p0 = kj < (hp ? Vi.z : Vi.x) ? p0 : 0.f;
