@@ -113,14 +113,25 @@ __global__ void __launch_bounds__(256) bwd_prep_kernel(
 
 // ------------------------------------------------------------------ dq
 namespace dq {
-constexpr uint32_t OFF_Q = 0, OFF_DO = TILE, OFF_K = 2 * TILE, OFF_V = 4 * TILE, OFF_DS = 6 * TILE;
-constexpr uint32_t OFF_BAR = 7 * TILE;
-enum { B_QD = 0, B_KF = 1, B_KE = 3, B_VF = 5, B_VE = 7, B_SF = 9, B_SE = 10, B_DSF = 11, B_DSE = 12, B_N = 13 };
+// K ring 3 deep: K_j is held until dQ_j completes, which is just before
+// S_{j+2} needs K_{j+2} (a 2-deep ring exposed the TMA latency there); V_j is
+// free once dP_j is done, so 2 stages suffice.
+constexpr int NSK = 3;
+constexpr uint32_t OFF_Q = 0, OFF_DO = TILE, OFF_K = 2 * TILE, OFF_V = OFF_K + NSK * TILE;
+constexpr uint32_t OFF_BAR = OFF_V + 2 * TILE;
+enum { B_QD = 0, B_KF = 1, B_KE = 1 + NSK, B_VF = 1 + 2 * NSK, B_VE = 3 + 2 * NSK, B_SF = 5 + 2 * NSK, B_SE, B_DSF,
+       B_DSE, B_N };
 constexpr uint32_t OFF_TMEM = OFF_BAR + 8 * B_N;
 constexpr uint32_t SMEM = OFF_TMEM + 16 + 1024;
-constexpr uint32_t COL_S = 0, COL_DP = 128, COL_DQ = 256;
+// dS (bf16 pairs, 64 columns) lives in TMEM: dQ += dS K is a TS MMA, so
+// the only shared-memory operand traffic of a key tile is S / dP's and K's
+// (the SS dS product made the kernel shared-memory-bandwidth bound)
+constexpr uint32_t COL_S = 0, COL_DP = 128, COL_DQ = 256, COL_DS = 384;
 }  // namespace dq
 
+// PROBE (profiling only, OMNI_DQ_PROBE=1): the gradient warps release dS
+// without computing it (the MMA / TMA pipeline floor).
+template <int PROBE>
 __global__ void __launch_bounds__(576, 1)
 dq_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
           const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
@@ -152,9 +163,11 @@ dq_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
     tma_prefetch_desc(&tm_k);
     tma_prefetch_desc(&tm_v);
     mbar_init(B(B_QD), 1);
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < NSK; ++s) {
       mbar_init(B(B_KF + s), 1);
       mbar_init(B(B_KE + s), 1);
+    }
+    for (int s = 0; s < 2; ++s) {
       mbar_init(B(B_VF + s), 1);
       mbar_init(B(B_VE + s), 1);
     }
@@ -183,11 +196,11 @@ dq_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
       tma_load_2d(sb + OFF_DO + ATOM, &tm_do, B(B_QD), 64, (int)crow0);
       const int kr0 = g * cap;
       for (int j = 0; j < nt; ++j) {
-        const int s = j & 1;
-        if (j >= 2) mbar_wait(B(B_KE + s), ((j >> 1) - 1) & 1);
-        mbar_expect_tx(B(B_KF + s), TILE);
-        tma_load_2d(sb + OFF_K + s * TILE, &tm_k, B(B_KF + s), 0, kr0 + j * 128);
-        tma_load_2d(sb + OFF_K + s * TILE + ATOM, &tm_k, B(B_KF + s), 64, kr0 + j * 128);
+        const int sk = j % NSK, s = j & 1;
+        if (j >= NSK) mbar_wait(B(B_KE + sk), ((j / NSK) - 1) & 1);
+        mbar_expect_tx(B(B_KF + sk), TILE);
+        tma_load_2d(sb + OFF_K + sk * TILE, &tm_k, B(B_KF + sk), 0, kr0 + j * 128);
+        tma_load_2d(sb + OFF_K + sk * TILE + ATOM, &tm_k, B(B_KF + sk), 64, kr0 + j * 128);
         if (j >= 2) mbar_wait(B(B_VE + s), ((j >> 1) - 1) & 1);
         mbar_expect_tx(B(B_VF + s), TILE);
         tma_load_2d(sb + OFF_V + s * TILE, &tm_v, B(B_VF + s), 0, kr0 + j * 128);
@@ -201,16 +214,16 @@ dq_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
       constexpr uint32_t id_mn = idesc_bf16_f32(128, 128, 0, 1);
       const uint64_t dq0 = sdesc_sw128(sb + OFF_Q, 16, 1024), ddo0 = sdesc_sw128(sb + OFF_DO, 16, 1024);
       const uint64_t dk0 = sdesc_sw128(sb + OFF_K, 16, 1024), dv0 = sdesc_sw128(sb + OFF_V, 16, 1024);
-      const uint64_t dds0 = sdesc_sw128(sb + OFF_DS, 16, 1024), dkmn0 = sdesc_sw128(sb + OFF_K, ATOM, 1024);
+      const uint64_t dkmn0 = sdesc_sw128(sb + OFF_K, ATOM, 1024);
       auto issue_s = [&](int j) {
-        const int s = j & 1;
-        mbar_wait(B(B_KF + s), (j >> 1) & 1);
+        const int s = j & 1, sk = j % NSK;
+        mbar_wait(B(B_KF + sk), (j / NSK) & 1);
         mbar_wait(B(B_VF + s), (j >> 1) & 1);
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
           const uint32_t off = ((kk >> 2) * ATOM + (kk & 3) * 32) >> 4;
-          umma_bf16_ws(tmem + COL_S, dq0 + off, dk0 + ((s * TILE) >> 4) + off, id_kk, kk > 0);
+          umma_bf16_ws(tmem + COL_S, dq0 + off, dk0 + ((sk * TILE) >> 4) + off, id_kk, kk > 0);
         }
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
@@ -227,13 +240,13 @@ dq_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
         if (j + 1 < nt) issue_s(j + 1);
         mbar_wait(B(B_DSF), j & 1);
         tc_fence_after();
-        const uint64_t kb = dkmn0 + (((j & 1) * TILE) >> 4);
+        const uint64_t kb = dkmn0 + (((j % NSK) * TILE) >> 4);
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
-          umma_bf16_ws(tmem + COL_DQ, dds0 + (((kk >> 2) * ATOM + (kk & 3) * 32) >> 4), kb + ((kk * 2048) >> 4),
+          umma_bf16_ts_ws(tmem + COL_DQ, tmem + COL_DS + kk * 8, kb + ((kk * 2048) >> 4),
                        id_mn, (j > 0 || kk > 0) ? 1u : 0u);
         }
-        umma_commit_ws(B(B_KE + (j & 1)));
+        umma_commit_ws(B(B_KE + j % NSK));
         umma_commit_ws(B(B_DSE));
       }
     }
@@ -253,7 +266,6 @@ dq_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
     const float sl2 = static_cast<float>(kLog2e / sqrt(static_cast<double>(D)));
     const uint64_t c2 = f32x2(sl2, sl2), nl2 = f32x2(-l2, -l2), nD2 = f32x2(-Dv, -Dv);
     const Exp2PolyConsts pc = exp2_poly_consts();
-    uint8_t* ds_gen = smem + OFF_DS;
     for (int j = 0; j < nt; ++j) {
       mbar_wait(B(B_SF), j & 1);
       tc_fence_after();
@@ -264,6 +276,11 @@ dq_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
       tmem_wait_ld();
       tc_fence_before();
       mbar_arrive(B(B_SE));  // S / dP of this tile consumed: the next tile's MMAs may overwrite them
+      if constexpr (PROBE == 1) {
+        if (j > 0) mbar_wait(B(B_DSE), (j - 1) & 1);
+        mbar_arrive(B(B_DSF));
+        continue;
+      }
       const int lim = vis - j * 128;
       // paired FP32 ops: x = s log2e/sqrt(d) - lse2, dS = 2^x (dP - D); the
       // visibility compare only on staircase tiles
@@ -294,13 +311,13 @@ dq_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
       };
       if (full) math(std::true_type{}); else math(std::false_type{});
       if (j > 0) mbar_wait(B(B_DSE), (j - 1) & 1);  // dQ MMA of j-1 finished reading dS
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int chunk = hf * 4 + q;  // 16-byte chunk index along keys (0..15)
-        *reinterpret_cast<uint4*>(ds_gen + (chunk >> 3) * ATOM + swz(i, chunk & 7)) =
-            make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
-      }
-      fence_proxy_async_smem();
+      tc_fence_after();
+      // dS of keys [cb, cb + 32) as 16 packed columns: keys 16kk .. 16kk + 15
+      // are TMEM columns COL_DS + 8kk, the A operand of dQ K-step kk
+      __syncwarp();
+      tmem_st16(tl + COL_DS + hf * 16, pk);
+      tmem_wait_st();
+      tc_fence_before();
       mbar_arrive(B(B_DSF));
     }
     if (nt > 0) {
@@ -991,12 +1008,17 @@ extern "C" int omni_sparse_attn_bwd(const void* Q, const void* K_sel, const void
   if ((rc = omni_make_tmap_rows(&tv, V_sel, (uint64_t)n_kv_heads * cap, 128, 2, 64, 128))) return rc;
   static bool attr = false;
   if (!attr) {
-    OMNI_CUDA_TRY(cudaFuncSetAttribute(bwd::dq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bwd::dq::SMEM));
+    OMNI_CUDA_TRY(cudaFuncSetAttribute(bwd::dq_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bwd::dq::SMEM));
+    OMNI_CUDA_TRY(cudaFuncSetAttribute(bwd::dq_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bwd::dq::SMEM));
     OMNI_CUDA_TRY(cudaFuncSetAttribute(bwd::dkv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bwd::dkv::SMEM));
     attr = true;
   }
   const int n_tiles = capq / 128;
-  bwd::dq_kernel<<<n_tiles * n_q_heads, 576, bwd::dq::SMEM, st>>>(tq128, tdo128, tk, tv, rows, counts, lse2c, Dc,
+  static const int dq_probe = [] {
+    const char* e = getenv("OMNI_DQ_PROBE");
+    return e ? atoi(e) : 0;
+  }();
+  (dq_probe == 1 ? bwd::dq_kernel<1> : bwd::dq_kernel<0>)<<<n_tiles * n_q_heads, 576, bwd::dq::SMEM, st>>>(tq128, tdo128, tk, tv, rows, counts, lse2c, Dc,
                                                                     visc, n_q_heads, rep, seq_len, cap, capq, n_tiles,
                                                                     dQ);
   if ((rc = omni_launch_check())) return rc;
