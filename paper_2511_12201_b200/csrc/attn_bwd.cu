@@ -740,9 +740,12 @@ dkv2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
       const uint64_t dk0 = sdesc_sw128(sb + OFF_K, 16, 1024), dv0 = sdesc_sw128(sb + OFF_V, 16, 1024);
       const uint64_t dq0 = sdesc_sw128(sb + OFF_Q, 16, 1024), ddo0 = sdesc_sw128(sb + OFF_DO, 16, 1024);
       const uint64_t dqm0 = sdesc_sw128(sb + OFF_Q, ATOM, 1024), ddom0 = sdesc_sw128(sb + OFF_DO, ATOM, 1024);
+      uint32_t tw_qf = 0;
       auto issue_st = [&](int k) {  // S^T(k) = K Q(k)^T -> COL_S
         const int s = k & 1;
+        const uint32_t q0 = clock();
         mbar_wait(B(B_QF + s), (k >> 1) & 1);
+        if constexpr (PROBE == 3) tw_qf += clock() - q0;
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
@@ -797,6 +800,7 @@ dkv2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
         if (lane == 0) {
           atomicAdd(&g_bwd_trace[4], (unsigned long long)tw_se);
           (void)tw_pf;
+          atomicAdd(&g_bwd_trace[3], (unsigned long long)tw_qf);  // (overrides the gradient st slot)
           atomicAdd(&g_bwd_trace[7], (unsigned long long)total);
         }
       }
@@ -917,7 +921,7 @@ dkv2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
     }
     if constexpr (PROBE == 3) {
       if (lane == 0) {
-        for (int q = 0; q < 4; ++q) atomicAdd(&g_bwd_trace[q], (unsigned long long)tg[q]);
+        for (int q = 0; q < 3; ++q) atomicAdd(&g_bwd_trace[q], (unsigned long long)tg[q]);
         atomicAdd(&g_bwd_trace[6], (unsigned long long)total);
         atomicAdd(&g_bwd_trace[5], (unsigned long long)tg[4]);  // (overrides the MMA PF wait slot)
       }
