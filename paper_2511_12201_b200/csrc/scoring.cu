@@ -145,9 +145,26 @@ __global__ void probe_finish_kernel(const T* __restrict__ K, int N, int d, int n
 // sums for the pooled query stay in registers until the end.
 constexpr int QS_U = 4;
 
+// query_select.py:63-68: active iff p_act > tau with p_act the max-subtracted
+// two-way softmax of (l0, l1). p is monotone in delta = l1 - l0, so away from
+// the boundary the decision is delta > T = ln(tau / (1 - tau)) without the
+// float64 exponential; within 1e-9 of T (the computed p can only disagree
+// within ~1e-14) and whenever p itself is wanted, the reference's expression
+// decides. Both paths use the same rounded l0 - l1, so decisions are
+// identical to evaluating the expression for every row.
+__device__ __forceinline__ int two_way_active(double l0, double l1, double tau, double T, double* p_out) {
+  if (p_out == nullptr && tau > 0.0) {
+    const double dlt = (l1 - l0) - T;
+    if (fabs(dlt) > 1e-9 * (1.0 + fabs(T))) return dlt > 0.0 ? 1 : 0;
+  }
+  const double p = (l1 >= l0) ? 1.0 / (exp(l0 - l1) + 1.0) : (exp(l1 - l0) / (1.0 + exp(l1 - l0)));
+  if (p_out) *p_out = p;
+  return (p > tau) ? 1 : 0;
+}
+
 template <typename T>
 __global__ void __launch_bounds__(256) q_score_kernel(const T* __restrict__ Q, int N, int d, int rep, int n_vision,
-                                                      double tau, int preserve, int block,
+                                                      double tau, double tau_logit, int preserve, int block,
                                                       const double* __restrict__ k_lazy,
                                                       const double* __restrict__ k_act, uint8_t* __restrict__ active,
                                                       double* __restrict__ p_act, double* __restrict__ pooled_q,
@@ -213,9 +230,7 @@ __global__ void __launch_bounds__(256) q_score_kernel(const T* __restrict__ Q, i
       if (r_mine < n_vision) {
         l0 *= scale;
         l1 *= scale;
-        const double p = (l1 >= l0) ? 1.0 / (exp(l0 - l1) + 1.0) : (exp(l1 - l0) / (1.0 + exp(l1 - l0)));
-        my_act = (p > tau) ? 1 : 0;
-        if (p_act) p_act[(size_t)h * n_vision + r_mine] = p;
+        my_act = two_way_active(l0, l1, tau, tau_logit, p_act ? p_act + (size_t)h * n_vision + r_mine : nullptr);
       }
       if (preserve && h == 0) my_act = 1;
       active[(size_t)h * N + r_mine] = static_cast<uint8_t>(my_act);
@@ -268,7 +283,8 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
 }
 
 __global__ void __launch_bounds__(256, 3) q_score_bulk_kernel(const __nv_bfloat16* __restrict__ Q, int N, int rep,
-                                                               int n_vision, double tau, int preserve, int block,
+                                                               int n_vision, double tau, double tau_logit,
+                                                               int preserve, int block,
                                                                const double* __restrict__ k_lazy,
                                                                const double* __restrict__ k_act,
                                                                uint8_t* __restrict__ active, double* __restrict__ p_act,
@@ -359,10 +375,7 @@ __global__ void __launch_bounds__(256, 3) q_score_bulk_kernel(const __nv_bfloat1
     if (fin) {
       if (r < n_vision) {
         const double l0 = sl * scale, l1 = sa * scale;
-        // max-subtracted two-way softmax (query_select.py:63-68)
-        const double p = (l1 >= l0) ? 1.0 / (exp(l0 - l1) + 1.0) : (exp(l1 - l0) / (1.0 + exp(l1 - l0)));
-        act = (p > tau) ? 1 : 0;
-        if (p_act) p_act[(size_t)h * n_vision + r] = p;
+        act = two_way_active(l0, l1, tau, tau_logit, p_act ? p_act + (size_t)h * n_vision + r : nullptr);
       }
       if (preserve && h == 0) act = 1;
       active[(size_t)h * N + r] = static_cast<uint8_t>(act);
@@ -560,6 +573,7 @@ extern "C" int omni_q_score(const void* Q, int dtype, int n_q_heads, int n_kv_he
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   dim3 grid(nblocks(seq_len, block_size), n_q_heads);
   const int rep = n_q_heads / n_kv_heads;
+  const double T = tau > 0.0 ? log(tau / (1.0 - tau)) : -INFINITY;  // decision threshold on l1 - l0
   __nv_bfloat16* oz = static_cast<__nv_bfloat16*>(O_zero);
   if (dtype == OMNI_DTYPE_BF16 && head_dim == 128 && block_size >= 64 && block_size <= QSB_MAX_ROWS) {
     const int shm = block_size * head_dim * 2;
@@ -568,15 +582,15 @@ extern "C" int omni_q_score(const void* Q, int dtype, int n_q_heads, int n_kv_he
       OMNI_CUDA_TRY(cudaFuncSetAttribute(q_score_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, shm));
       attr = shm;
     }
-    q_score_bulk_kernel<<<grid, 256, shm, s>>>(static_cast<const __nv_bfloat16*>(Q), seq_len, rep, n_vision, tau,
+    q_score_bulk_kernel<<<grid, 256, shm, s>>>(static_cast<const __nv_bfloat16*>(Q), seq_len, rep, n_vision, tau, T,
                                                preserve_first_head, block_size, k_lazy, k_act, active, p_act, pooled_q,
                                                block_active, oz);
   } else if (dtype == OMNI_DTYPE_BF16)
     q_score_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(Q), seq_len, head_dim, rep,
-                                                       n_vision, tau, preserve_first_head, block_size, k_lazy, k_act,
-                                                       active, p_act, pooled_q, block_active, oz);
+                                                       n_vision, tau, T, preserve_first_head, block_size, k_lazy,
+                                                       k_act, active, p_act, pooled_q, block_active, oz);
   else if (dtype == OMNI_DTYPE_F32)
-    q_score_kernel<float><<<grid, 256, 0, s>>>(static_cast<const float*>(Q), seq_len, head_dim, rep, n_vision, tau,
+    q_score_kernel<float><<<grid, 256, 0, s>>>(static_cast<const float*>(Q), seq_len, head_dim, rep, n_vision, tau, T,
                                                preserve_first_head, block_size, k_lazy, k_act, active, p_act,
                                                pooled_q, block_active, oz);
   else
