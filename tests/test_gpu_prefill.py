@@ -224,3 +224,26 @@ def test_exact_score_source_c1_end_to_end():
     for g in range(4):
         np.testing.assert_array_equal(sel[g, : ref.budget], ref.selected[g])
     check_outputs(res, Q, K, V, ref, heads=[0, 3])
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+def test_q_score_decision_at_the_boundary(dtype):
+    """K2 decides far from the boundary on l1 - l0 vs ln(tau/(1-tau)) and
+    evaluates the reference expression (query_select.py:63-68) near it. With
+    tau set to rows' own computed p_act (the hardest ties: p > tau is false
+    for exactly those rows), the flags equal p > tau for every row."""
+    from paper_2511_12201_b200 import ops
+
+    Q, K, V = generate(Spec(heads=4, heads_kv=2, head_dim=128, n_vision=3000, n_text=40, seed=11))
+    Qd, Kd = to_dev(round_bf16(Q), dtype), to_dev(round_bf16(K), dtype)
+    kl, ka, _ = ops.kv_probe(Kd, 3000, 0, 256)
+    _, p, _, _ = ops.q_score(Qd, kl, ka, 3000, 0.08, False, 256, want_prob=True)
+    p = p.cpu().numpy()
+    for r in (5, 777, 2999):
+        tau = float(p[1, r])
+        if not 0.0 < tau < 1.0:
+            continue
+        act, _, _, _ = ops.q_score(Qd, kl, ka, 3000, tau, False, 256)
+        got = act.cpu().numpy()[:, :3000].astype(bool)
+        np.testing.assert_array_equal(got, p > tau)
+        assert not got[1, r]
