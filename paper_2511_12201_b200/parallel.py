@@ -2,7 +2,7 @@
 
 SURVEY §8e: work shards by KV group. A rank owns a contiguous range of KV
 groups (world <= Hkv) or a contiguous slice of one group's Q heads (world >
-Hkv, e.g. 8 GPUs over 4 groups: 4 + 3 Q heads per rank with the group's K/V
+Hkv, e.g. 8 GPUs over 4 groups: 3 + 4 Q heads per rank with the group's K/V
 replicated). K1/K2/K3a run locally; the only exchange is ONE all_gather of
 the per-Q-head block column masses (28 x nb x 8 B = 57 KB at 64K), after
 which every rank redundantly runs the selection (flattest group, budget,
@@ -61,8 +61,14 @@ def shard_plan(n_q_heads: int, n_kv_heads: int, world: int, rank: int) -> ShardP
     g = rank // per_group
     part = rank % per_group
     base, extra = divmod(rep, per_group)
-    start = part * base + min(part, extra)
-    stop = start + base + (1 if part < extra else 0)
+    # the extra heads go to the LAST parts of a group: the first part of
+    # group 0 holds Q head 0, which preserve_first_head keeps fully active
+    # (about twice a lazy-masked head's work), so it takes one head fewer
+    # (8 GPUs, 28/4 heads: 3 + 4 per group, max per-rank work 4 head-units
+    # instead of 5)
+    lead = per_group - extra
+    start = part * base + max(0, part - lead)
+    stop = start + base + (1 if part >= lead else 0)
     return ShardPlan(g * rep + start, g * rep + stop, g, g + 1, n_q_heads, n_kv_heads)
 
 
