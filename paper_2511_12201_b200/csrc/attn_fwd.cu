@@ -355,7 +355,9 @@ sparse_fwd_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constan
           return rs;
         };
         // FAST path chunk: exponentials against the shared running max only.
-        auto chunk_fast = [&](int q, float m_cur, float& cmax) -> float {
+        // No chunk maximum: every P <= 2^8 unless the half-row sum exceeds
+        // 2^8, and log2 of the sum bounds the growth when it does.
+        auto chunk_fast = [&](int q, float m_cur) -> float {
           uint32_t sr[32], pk[16];
           __syncwarp();
           tmem_ld32(tl + col_s(x) + cb + q * 32, sr);
@@ -365,14 +367,7 @@ sparse_fwd_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constan
             for (int c = 0; c < 32; ++c)
               if (q * 32 + c >= lim) sr[c] = __float_as_uint(-INFINITY);
           }
-          float m0 = -INFINITY, m1 = -INFINITY;
-#pragma unroll
-          for (int c = 0; c < 32; c += 4) {
-            m0 = fmax3(m0, __uint_as_float(sr[c]), __uint_as_float(sr[c + 1]));
-            m1 = fmax3(m1, __uint_as_float(sr[c + 2]), __uint_as_float(sr[c + 3]));
-          }
           const float rs = full ? exps(std::true_type{}, sr, -m_cur, pk) : exps(std::false_type{}, sr, -m_cur, pk);
-          cmax = fmaxf(cmax, fmaxf(m0, m1) * sl2);
           tmem_st16(tl + col_s(x) + cb + q * 16, pk);
           return rs;
         };
@@ -400,15 +395,14 @@ sparse_fwd_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constan
             }
           }
           if (!__any_sync(0xffffffffu, m_run == -INFINITY && lim_row > 0)) {
-            float cmax = -INFINITY, mu0, mu1;
-            float m_cur = m_run;
-            const float rs = chunk_fast(0, m_cur, cmax) + chunk_fast(1, m_cur, cmax);
-            (void)mu0; (void)mu1;
+            const float rs = chunk_fast(0, m_run) + chunk_fast(1, m_run);
             tmem_wait_st();
             tc_fence_before();
             mbar_arrive(B(B_PF + x));
-            if (cmax > m_run + 64.0f) atomicExch(status, 1);
-            const float tgt = cmax > m_run + 8.0f ? ceilf(cmax) : m_run;
+            // rows that have seen no visible key yet (m_run = -inf; their
+            // masked P are NaN and never used) are excluded from both tests
+            if (m_run != -INFINITY && !(rs <= 0x1p64f)) atomicExch(status, 1);  // some P may exceed 2^64
+            const float tgt = (m_run != -INFINITY && rs > 256.f) ? m_run + ceilf(__log2f(rs)) : m_run;
             if (named_bar_red_or(bid, 2 * 32, tgt != m_run)) {
               s_xch[x][i][hf] = tgt;
               named_bar_sync(bid, 2 * 32);

@@ -1,5 +1,5 @@
 # A/B of two prebuilt variants (library + Python binding) on the same box
-for r in 1 2; do
+for r in 1 2 3 4; do
 for v in base new; do
   cp profiles/micro/ab/lib_$v.so paper_2511_12201_b200/lib/libomnisparse.so
   cp profiles/micro/ab/ops_$v.py paper_2511_12201_b200/ops.py
