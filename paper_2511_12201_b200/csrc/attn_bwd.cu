@@ -636,7 +636,8 @@ constexpr uint32_t OFF_K = 0, OFF_V = TILE, OFF_Q = 2 * TILE, OFF_DO = 4 * TILE;
 constexpr int NI = 4;                                                             // row-info ring depth
 constexpr uint32_t OFF_INFO = 6 * TILE;                                           // [NI][3][128]
 constexpr uint32_t OFF_BAR = OFF_INFO + NI * 3 * BR * 4;
-enum { B_KV = 0, B_QF = 1, B_QE = 3, B_IF = 5, B_IE = 5 + NI, B_SF = 5 + 2 * NI, B_SE, B_PF, B_PE, B_N };
+// B_TF: S^T(k) ready; B_SF: dP^T(k) ready; B_SE: S^T(k) read by every gradient thread
+enum { B_KV = 0, B_QF = 1, B_QE = 3, B_IF = 5, B_IE = 5 + NI, B_SF = 5 + 2 * NI, B_SE, B_PF, B_PE, B_TF, B_N };
 constexpr uint32_t OFF_TMEM = OFF_BAR + 8 * B_N;
 constexpr uint32_t SMEM = OFF_TMEM + 16 + 1024;
 constexpr uint32_t COL_S = 0, COL_DP = 128, COL_DV = 256, COL_DK = 384;
@@ -698,6 +699,7 @@ dkv2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
       mbar_init(B(B_IE + s), 512);
     }
     mbar_init(B(B_SF), 1);
+    mbar_init(B(B_TF), 1);
     mbar_init(B(B_SE), 512);
     mbar_init(B(B_PF), 512);
     mbar_init(B(B_PE), 1);
@@ -752,6 +754,7 @@ dkv2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
           const uint32_t off = ((kk >> 2) * ATOM + (kk & 3) * 32) >> 4;
           umma_bf16_ws(tmem + COL_S, dk0 + off, dq0 + ((s * TILE) >> 4) + off, id_s, kk > 0);
         }
+        umma_commit_ws(B(B_TF));
       };
       auto issue_dpt = [&](int k) {  // dP^T(k) = V dO(k)^T -> COL_DP
         const int s = k & 1;
@@ -769,7 +772,7 @@ dkv2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
       for (int k = 0; k < total; ++k) {
         const int s = k & 1;
         const uint32_t t0 = clock();
-        mbar_wait(B(B_SE), k & 1);  // S^T(k), dP^T(k) read by every gradient thread
+        mbar_wait(B(B_SE), k & 1);  // S^T(k) read by every gradient thread
         tc_fence_after();
         const uint32_t t1 = clock();
         if (k + 1 < total) issue_st(k + 1);
@@ -832,14 +835,16 @@ dkv2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
     const int cb = cq * 32;
     uint32_t tg[5] = {0, 0, 0, 0, 0};
     for (int k = 0; k < total; ++k) {
+      // Two phases: P^T from S^T as soon as S^T(k) is ready — it overlaps
+      // dV / dK(k-1) and dP^T(k) on the tensor core — then only the cheap
+      // dS^T = P^T (dP^T - D) waits for dP^T(k).
       const uint32_t c0 = clock();
-      mbar_wait(B(B_SF), k & 1);
+      mbar_wait(B(B_TF), k & 1);
       tc_fence_after();
       const uint32_t c1 = clock();
-      uint32_t sv[32], dp[32];
+      uint32_t sv[32];
       __syncwarp();
       tmem_ld32(tl + COL_S + cb, sv);
-      tmem_ld32(tl + COL_DP + cb, dp);
       tmem_wait_ld();
       const uint32_t c2c = clock();
       tc_fence_before();
@@ -847,6 +852,7 @@ dkv2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
       if constexpr (PROBE == 1) {
         mbar_wait(B(B_IF + k % NI), (k / NI) & 1);
         mbar_arrive(B(B_IE + k % NI));
+        mbar_wait(B(B_SF), k & 1);
         mbar_arrive(B(B_PF));
         continue;
       }
@@ -864,13 +870,13 @@ dkv2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
       const uint64_t c2 = f32x2(sl2, sl2);
       const Exp2PolyConsts pc = exp2_poly_consts();
       uint32_t pp[16], pd[16];
-      // separate instantiations for full and staircase tiles: predicated-off
-      // selects would still take issue slots (the loop is issue-bound)
-      auto math = [&](auto full_c) {
+      // phase 1 (P^T, bf16 pairs). Separate instantiations for full and
+      // staircase tiles: predicated-off selects would still take issue slots
+      auto pmath = [&](auto full_c) {
         constexpr bool FULL = decltype(full_c)::value;
 #pragma unroll
         for (int c4 = 0; c4 < 8; ++c4) {
-          const float4 L = lds_f4(a_l2 + 16 * c4), Dn = lds_f4(a_dd + 16 * c4);
+          const float4 L = lds_f4(a_l2 + 16 * c4);
           int4 Vi;
           if constexpr (!FULL) Vi = lds_i4(a_vv + 16 * c4);
 #pragma unroll
@@ -893,14 +899,31 @@ dkv2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
               p0 = kj < (hp ? Vi.z : Vi.x) ? p0 : 0.f;
               p1 = kj < (hp ? Vi.w : Vi.y) ? p1 : 0.f;
             }
-            const uint64_t ds = fmul2(f32x2(p0, p1), fadd2(f32x2(__uint_as_float(dp[c]), __uint_as_float(dp[c + 1])),
-                                                             hp ? f32x2(Dn.z, Dn.w) : f32x2(Dn.x, Dn.y)));
             pp[c / 2] = pack_bf16x2(p0, p1);
-            pd[c / 2] = pack_bf16x2(f32x2_lo(ds), f32x2_hi(ds));
           }
         }
       };
-      if (full) math(std::true_type{}); else math(std::false_type{});
+      if (full) pmath(std::true_type{}); else pmath(std::false_type{});
+      // phase 2: dS^T = P^T (dP^T - D) with the bf16 P^T (the values dV uses)
+      mbar_wait(B(B_SF), k & 1);
+      tc_fence_after();
+      uint32_t dp[32];
+      __syncwarp();
+      tmem_ld32(tl + COL_DP + cb, dp);
+      tmem_wait_ld();
+#pragma unroll
+      for (int c4 = 0; c4 < 8; ++c4) {
+        const float4 Dn = lds_f4(a_dd + 16 * c4);
+#pragma unroll
+        for (int hp = 0; hp < 2; ++hp) {
+          const int c = 4 * c4 + 2 * hp;
+          const uint32_t w = pp[c / 2];
+          const uint64_t pv = f32x2(__uint_as_float(w << 16), __uint_as_float(w & 0xFFFF0000u));
+          const uint64_t ds = fmul2(pv, fadd2(f32x2(__uint_as_float(dp[c]), __uint_as_float(dp[c + 1])),
+                                              hp ? f32x2(Dn.z, Dn.w) : f32x2(Dn.x, Dn.y)));
+          pd[c / 2] = pack_bf16x2(f32x2_lo(ds), f32x2_hi(ds));
+        }
+      }
       mbar_arrive(B(B_IE + si));
       const uint32_t c3 = clock();
       // P^T / dS^T over this thread's own (already read) dP^T columns; dV / dK(k-1)
