@@ -90,17 +90,17 @@ __device__ unsigned long long g_fwd_trace[8];
 // FAST: deferred agreement between the two halves of a row (see the tile loop);
 // a tile whose logits jump by more than 2^64 over the running max sets
 // *status and the launch is redone by the FAST = false kernel (only_if).
-template <int POLY, bool TRACE = false, bool FAST = false>
-__global__ void __launch_bounds__(NTHREADS, 1)
-sparse_fwd_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
-                  const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __restrict__ Vorig,
-                  const int32_t* __restrict__ rows, const int32_t* __restrict__ counts,
-                  const int32_t* __restrict__ sel, const int32_t* __restrict__ sel_counts, int Hq, int rep, int N,
-                  int cap, int sel_stride, int sink, int n_tiles_max, __nv_bfloat16* __restrict__ O,
-                  float* __restrict__ lse, int* __restrict__ status, const int* __restrict__ only_if) {
-  if (only_if != nullptr && *(volatile const int*)only_if == 0) return;  // fallback launch not needed
+// One CTA's work: 256 compacted rows (tile pair L) of one Q head. `reuse`:
+// the CTA runs further tiles after this one (mbarriers invalidated at exit).
+template <int POLY, bool TRACE, bool FAST>
+__device__ __forceinline__ void fwd_tile(int L, bool reuse, const CUtensorMap& tm_k, const CUtensorMap& tm_v,
+                                         const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __restrict__ Vorig,
+                                         const int32_t* __restrict__ rows, const int32_t* __restrict__ counts,
+                                         const int32_t* __restrict__ sel, const int32_t* __restrict__ sel_counts,
+                                         int Hq, int rep, int N, int cap, int sel_stride, int sink, int n_tiles_max,
+                                         __nv_bfloat16* __restrict__ O, float* __restrict__ lse,
+                                         int* __restrict__ status) {
   extern __shared__ uint8_t smem_raw[];
-  const int L = blockIdx.x;
   const int h = L % Hq;
   const int tile = n_tiles_max - 1 - L / Hq;  // heaviest (latest rows) tiles first
   const int cnt = __ldg(counts + h);
@@ -161,7 +161,7 @@ sparse_fwd_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constan
   }
   if (warp == 1) {
     tmem_alloc(smem_u32(tmem_slot), TMEM_COLS);
-    tmem_relinquish();
+    if (!reuse) tmem_relinquish();  // a reusing CTA allocates again for its next tile
   }
   tc_fence_before();
   __syncthreads();
@@ -526,6 +526,35 @@ sparse_fwd_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constan
     tc_fence_after();
     tmem_dealloc(tmem, TMEM_COLS);
   }
+  if (reuse) {  // the next tile re-initialises the barriers
+    __syncthreads();
+    if (threadIdx.x == 0)
+      for (int k = 0; k < B_COUNT; ++k) mbar_inval(B(k));
+    __syncthreads();
+  }
+}
+
+// REDO: the fallback instance behind a FAST launch (only_if = its status word).
+template <int POLY, bool TRACE = false, bool FAST = false, bool REDO = false>
+__global__ void __launch_bounds__(NTHREADS, 1)
+sparse_fwd_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
+                  const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __restrict__ Vorig,
+                  const int32_t* __restrict__ rows, const int32_t* __restrict__ counts,
+                  const int32_t* __restrict__ sel, const int32_t* __restrict__ sel_counts, int Hq, int rep, int N,
+                  int cap, int sel_stride, int sink, int n_tiles_max, __nv_bfloat16* __restrict__ O,
+                  float* __restrict__ lse, int* __restrict__ status, const int* __restrict__ only_if) {
+  if constexpr (REDO) {
+    // fallback launch (one CTA per SM): nothing to do unless the fast kernel
+    // flagged a jump; then redo every tile pair, grid-stride
+    if (*(volatile const int*)only_if == 0) return;
+    const int total = n_tiles_max * Hq;
+    for (int L = blockIdx.x; L < total; L += gridDim.x)
+      fwd_tile<POLY, TRACE, false>(L, true, tm_k, tm_v, Q, Vorig, rows, counts, sel, sel_counts, Hq, rep, N, cap,
+                                   sel_stride, sink, n_tiles_max, O, lse, status);
+    return;
+  }
+  fwd_tile<POLY, TRACE, FAST>(blockIdx.x, false, tm_k, tm_v, Q, Vorig, rows, counts, sel, sel_counts, Hq, rep, N, cap,
+                              sel_stride, sink, n_tiles_max, O, lse, status);
 }
 
 }  // namespace fwd
@@ -604,6 +633,10 @@ extern "C" int omni_sparse_attn_fwd_ex(const void* Q, const void* K_sel, const v
             : poly == 8 ? fwd::sparse_fwd_kernel<8, false, true>
             : poly == 6 ? fwd::sparse_fwd_kernel<6, false, true>
                         : fwd::sparse_fwd_kernel<4, false, true>;
+  auto redo = poly == 0 ? fwd::sparse_fwd_kernel<0, false, false, true>
+            : poly == 8 ? fwd::sparse_fwd_kernel<8, false, false, true>
+            : poly == 6 ? fwd::sparse_fwd_kernel<6, false, false, true>
+                        : fwd::sparse_fwd_kernel<4, false, false, true>;
   const bool use_fast = status != nullptr && fast_env && !trace && poly >= 0;
   static bool attr_set[2] = {false, false};
   if (!attr_set[0]) {
@@ -612,6 +645,7 @@ extern "C" int omni_sparse_attn_fwd_ex(const void* Q, const void* K_sel, const v
   }
   if (use_fast && !attr_set[1]) {
     OMNI_CUDA_TRY(cudaFuncSetAttribute(fast, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fwd::SMEM_BYTES));
+    OMNI_CUDA_TRY(cudaFuncSetAttribute(redo, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fwd::SMEM_BYTES));
     attr_set[1] = true;
   }
   const int n_tiles = (seq_len + 2 * fwd::BM - 1) / (2 * fwd::BM);
@@ -625,9 +659,13 @@ extern "C" int omni_sparse_attn_fwd_ex(const void* Q, const void* K_sel, const v
     fast<<<grid, fwd::NTHREADS, fwd::SMEM_BYTES, st_>>>(tk, tv, qp, vp, rows, counts, selected, sel_counts, n_q_heads,
                                                         rep, seq_len, cap, seq_len, sink_index, n_tiles, op, lse,
                                                         status, nullptr);
-    safe<<<grid, fwd::NTHREADS, fwd::SMEM_BYTES, st_>>>(tk, tv, qp, vp, rows, counts, selected, sel_counts, n_q_heads,
-                                                        rep, seq_len, cap, seq_len, sink_index, n_tiles, op, lse,
-                                                        nullptr, status);
+    int dev = 0, sms = 148;
+    OMNI_CUDA_TRY(cudaGetDevice(&dev));
+    OMNI_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const dim3 fb_grid(std::min<unsigned>(grid.x, (unsigned)sms));  // exits at once in the common case
+    redo<<<fb_grid, fwd::NTHREADS, fwd::SMEM_BYTES, st_>>>(tk, tv, qp, vp, rows, counts, selected, sel_counts,
+                                                           n_q_heads, rep, seq_len, cap, seq_len, sink_index, n_tiles,
+                                                           op, lse, nullptr, status);
   } else {
     safe<<<grid, fwd::NTHREADS, fwd::SMEM_BYTES, st_>>>(tk, tv, qp, vp, rows, counts, selected, sel_counts, n_q_heads,
                                                         rep, seq_len, cap, seq_len, sink_index, n_tiles, op, lse,
