@@ -52,31 +52,77 @@ __device__ __forceinline__ void mma_bf16_16816(float* c, const uint32_t* a, uint
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
-__global__ void decode_flags_kernel(const __nv_bfloat16* __restrict__ q, const double* __restrict__ k_lazy,
-                                    const double* __restrict__ k_act, int Hq, int Hkv, double tau, int preserve,
-                                    const uint8_t* __restrict__ flags_override, uint8_t* __restrict__ flags) {
-  const int h = blockIdx.x, s = blockIdx.y, lane = threadIdx.x;
-  const int g = h / (Hq / Hkv);
+// Classification of the Q heads of KV group g of sequence s, one warp:
+// lane l takes head r = l / 4 and head dims (l % 4) * 32 .. +31 (float64,
+// query_select.py:63-68 with the decode probe keys), the four partial dots
+// meet in a 2-step butterfly (identical on the four lanes). Returns the
+// group's active mask (bit r = head g * rep + r) on every lane; head 0 is
+// forced active under preserve; flags_override (decode.py:170-173) wins.
+__device__ __forceinline__ uint32_t group_flag_mask(const __nv_bfloat16* __restrict__ q,
+                                                    const double* __restrict__ k_lazy,
+                                                    const double* __restrict__ k_act, int s, int g, int Hq, int Hkv,
+                                                    double tau, int preserve,
+                                                    const uint8_t* __restrict__ flags_override, double* sk) {
+  // sk: 2 x D doubles of shared memory owned by this warp (the group's probe
+  // keys, staged with coalesced loads so the float64 dot chains read them at
+  // shared-memory latency)
+  const int lane = threadIdx.x & 31, rep = Hq / Hkv;
+  const int r = lane >> 2, qd = (lane & 3) * 32;
+  const int h = g * rep + (r < rep ? r : 0);
+  int f = 0;
   if (flags_override) {
-    if (lane == 0) flags[(size_t)s * Hq + h] = flags_override[(size_t)s * Hq + h] ? 1 : 0;
-    return;
-  }
-  double dl = 0.0, da = 0.0;
-  for (int e = lane; e < D; e += 32) {
-    const double x = static_cast<double>(__bfloat162float(q[((size_t)s * Hq + h) * D + e]));
-    dl = fma(x, k_lazy[((size_t)s * Hkv + g) * D + e], dl);
-    da = fma(x, k_act[((size_t)s * Hkv + g) * D + e], da);
-  }
-  dl = warp_sum(dl);
-  da = warp_sum(da);
-  if (lane == 0) {
+    f = (r < rep && flags_override[(size_t)s * Hq + h]) ? 1 : 0;
+  } else {
+    uint4 qv[4];
+    const uint4* qp = reinterpret_cast<const uint4*>(q + ((size_t)s * Hq + h) * D + qd);
+#pragma unroll
+    for (int v = 0; v < 4; ++v) qv[v] = __ldg(qp + v);
+    {
+      const double2* kl2 = reinterpret_cast<const double2*>(k_lazy + ((size_t)s * Hkv + g) * D);
+      const double2* ka2 = reinterpret_cast<const double2*>(k_act + ((size_t)s * Hkv + g) * D);
+      double2 a = __ldg(kl2 + lane), b = __ldg(kl2 + 32 + lane), c = __ldg(ka2 + lane), d = __ldg(ka2 + 32 + lane);
+      __syncwarp();
+      reinterpret_cast<double2*>(sk)[lane] = a;
+      reinterpret_cast<double2*>(sk)[32 + lane] = b;
+      reinterpret_cast<double2*>(sk + D)[lane] = c;
+      reinterpret_cast<double2*>(sk + D)[32 + lane] = d;
+      __syncwarp();
+    }
+    double dl = 0.0, da = 0.0;
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const __nv_bfloat16* hv = reinterpret_cast<const __nv_bfloat16*>(&qv[v]);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const double x = static_cast<double>(__bfloat162float(hv[e]));
+        dl = fma(x, sk[qd + v * 8 + e], dl);
+        da = fma(x, sk[D + qd + v * 8 + e], da);
+      }
+    }
+    dl += __shfl_xor_sync(0xffffffffu, dl, 1);
+    da += __shfl_xor_sync(0xffffffffu, da, 1);
+    dl += __shfl_xor_sync(0xffffffffu, dl, 2);
+    da += __shfl_xor_sync(0xffffffffu, da, 2);
     const double scale = 1.0 / sqrt(static_cast<double>(D));
     const double l0 = dl * scale, l1 = da * scale, mx = fmax(l0, l1);
     const double e0 = exp(l0 - mx), e1 = exp(l1 - mx);
-    int f = (e1 / (e0 + e1) > tau) ? 1 : 0;
-    if (preserve && h == 0) f = 1;
-    flags[(size_t)s * Hq + h] = static_cast<uint8_t>(f);
+    f = (r < rep && e1 / (e0 + e1) > tau) ? 1 : 0;
+    if (preserve && h == 0 && r == 0) f = 1;
   }
+  const uint32_t b = __ballot_sync(0xffffffffu, f && (lane & 3) == 0);  // bit 4r
+  uint32_t mask = 0;
+#pragma unroll
+  for (int k = 0; k < MAXREP; ++k) mask |= ((b >> (4 * k)) & 1u) << k;
+  return mask;
+}
+
+__global__ void decode_flags_kernel(const __nv_bfloat16* __restrict__ q, const double* __restrict__ k_lazy,
+                                    const double* __restrict__ k_act, int Hq, int Hkv, double tau, int preserve,
+                                    const uint8_t* __restrict__ flags_override, uint8_t* __restrict__ flags) {
+  __shared__ __align__(16) double sk[2 * D];
+  const int g = blockIdx.x, s = blockIdx.y, lane = threadIdx.x, rep = Hq / Hkv;
+  const uint32_t mask = group_flag_mask(q, k_lazy, k_act, s, g, Hq, Hkv, tau, preserve, flags_override, sk);
+  if (lane < rep) flags[(size_t)s * Hq + g * rep + lane] = static_cast<uint8_t>((mask >> lane) & 1u);
 }
 
 __global__ void __launch_bounds__(128) decode_partial_kernel(
@@ -273,9 +319,11 @@ __global__ void decode_combine_kernel(const float* __restrict__ part_ml, const f
   const float* ml = part_ml + base * n_chunks * 2;
   const float* acc = part_acc + base * n_chunks * D;
   float M = -INFINITY;
+#pragma unroll 8
   for (int c = 0; c < n_chunks; ++c) M = fmaxf(M, ml[2 * c]);
   float L = 0.f, o = 0.f;
   const int col = threadIdx.x;
+#pragma unroll 8
   for (int c = 0; c < n_chunks; ++c) {
     const float m = ml[2 * c];
     if (m == -INFINITY) continue;
@@ -345,6 +393,24 @@ __device__ __forceinline__ DecItem dec_item(int t, int nc, int Hq, int Hkv, cons
   return it;
 }
 
+// FUSED: the item's key range from the group's active mask (computed by the
+// producer warp, handed to the consumers through a shared-memory ring)
+__device__ __forceinline__ DecItem dec_item_mask(int t, int nc, int Hkv, const SegLens& sl,
+                                                 const int32_t* __restrict__ vlen, uint32_t mask) {
+  DecItem it;
+  it.c = t % nc;
+  it.g = (t / nc) % Hkv;
+  it.s = t / (nc * Hkv);
+  it.any = mask != 0u;
+  it.vl = vlen[it.s];
+  it.nt = sl.text(it.s);
+  const int k_start = it.any ? 0 : it.vl;
+  const int k_end = it.vl + it.nt + sl.answer(it.s);
+  it.lo = k_start + it.c * CTA_KEYS;
+  it.hi = min(k_end, it.lo + CTA_KEYS);
+  return it;
+}
+
 // tile starting at key k of item `it`: segment, local row, valid keys
 __device__ __forceinline__ void dec_tile(const DecItem& it, int k, int& seg, int& row, int& nvalid) {
   const int nt = it.nt;
@@ -356,15 +422,35 @@ __device__ __forceinline__ void dec_tile(const DecItem& it, int k, int& seg, int
   nvalid = min(TK, min(seg_hi, it.hi) - k);
 }
 
+// FUSED (default): the producer warp classifies each item's Q heads
+// (group_flag_mask, the arithmetic of decode_flags_kernel) and hands the
+// item's active mask to the consumers through a small shared-memory ring —
+// no separate classification launch. (Merging the partials in the CTA that
+// finishes a group's last chunk measured 3.7x slower than the separate merge
+// kernel: the merge lands on few CTAs at the tail.)
+struct FuseArgs {
+  const double* k_lazy;
+  const double* k_act;
+  double tau;
+  int preserve;
+  const uint8_t* flags_override;
+  uint8_t* flags_out;
+};
+constexpr int NIT = 4;  // item ring depth
+
+template <bool FUSED>
 __global__ void __launch_bounds__((NCW + 1) * 32, 1) decode_partial_tma_kernel(
     const __grid_constant__ CUtensorMap tm_vk, const __grid_constant__ CUtensorMap tm_vv,
     const __grid_constant__ CUtensorMap tm_tk, const __grid_constant__ CUtensorMap tm_tv,
     const __grid_constant__ CUtensorMap tm_ak, const __grid_constant__ CUtensorMap tm_av,
     const __nv_bfloat16* __restrict__ q, const int32_t* __restrict__ vlen, SegLens sl, int Hq, int Hkv,
     int vcap, int acap, const uint8_t* __restrict__ flags, float* __restrict__ part_ml,
-    float* __restrict__ part_acc, int n_chunks, int total_items) {
+    float* __restrict__ part_acc, int n_chunks, int total_items, FuseArgs fa) {
   extern __shared__ uint8_t dsm_raw[];
   __shared__ __align__(8) uint64_t full_bar[NSTG], empty_bar[NSTG];
+  __shared__ __align__(8) uint64_t item_full[NIT], item_empty[NIT];
+  __shared__ uint32_t s_mask[NIT];
+  __shared__ __align__(16) double s_kstage[2 * D];  // producer: the item group's probe keys
   __shared__ float s_ml[NCW][MAXREP][2];
   __shared__ float s_acc[NCW][MAXREP][D];
   uint8_t* dsm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dsm_raw) + 1023) & ~uintptr_t(1023));
@@ -374,6 +460,10 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1) decode_partial_tma_kernel(
     for (int i = 0; i < NSTG; ++i) {
       mbar_init(smem_u32(&full_bar[i]), 1);
       mbar_init(smem_u32(&empty_bar[i]), NCW);
+    }
+    for (int i = 0; i < NIT; ++i) {
+      mbar_init(smem_u32(&item_full[i]), 1);
+      mbar_init(smem_u32(&item_empty[i]), NCW);
     }
     fence_mbar_init();
   }
@@ -386,9 +476,26 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1) decode_partial_tma_kernel(
       tma_prefetch_desc(&tm_vk); tma_prefetch_desc(&tm_vv);
       tma_prefetch_desc(&tm_tk); tma_prefetch_desc(&tm_tv);
       tma_prefetch_desc(&tm_ak); tma_prefetch_desc(&tm_av);
-      uint32_t n = 0;
-      for (int t = blockIdx.x; t < total_items; t += gridDim.x) {
-        const DecItem it = dec_item(t, n_chunks, Hq, Hkv, sl, vlen, flags);
+    }
+    uint32_t n = 0, ni = 0;
+    for (int t = blockIdx.x; t < total_items; t += gridDim.x, ++ni) {
+      DecItem it;
+      if constexpr (FUSED) {
+        const int s_ = t / (n_chunks * Hkv), g_ = (t / n_chunks) % Hkv;
+        const uint32_t mask = group_flag_mask(q, fa.k_lazy, fa.k_act, s_, g_, Hq, Hkv, fa.tau, fa.preserve,
+                                              fa.flags_override, s_kstage);
+        it = dec_item_mask(t, n_chunks, Hkv, sl, vlen, mask);
+        if (it.c == 0 && lane < rep) fa.flags_out[(size_t)it.s * Hq + it.g * rep + lane] = (mask >> lane) & 1u;
+        const int slot = ni % NIT;
+        if (ni >= NIT) mbar_wait(smem_u32(&item_empty[slot]), ((ni / NIT) - 1) & 1);
+        if (lane == 0) {
+          s_mask[slot] = mask;
+          mbar_arrive(smem_u32(&item_full[slot]));  // release: the mask write precedes it
+        }
+      } else {
+        it = dec_item(t, n_chunks, Hq, Hkv, sl, vlen, flags);
+      }
+      if (lane == 0) {
         const int sg = it.s * Hkv + it.g;
         for (int k = it.lo; k < it.hi; k += TK) {
           int seg, row, nv;
@@ -409,6 +516,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1) decode_partial_tma_kernel(
           ++n;
         }
       }
+      __syncwarp();
     }
     return;
   }
@@ -416,10 +524,22 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1) decode_partial_tma_kernel(
   const int r4 = lane & 3, gid = lane >> 2;
   const bool row_valid = gid < rep;
   const float sl2 = static_cast<float>(kLog2e / sqrt(static_cast<double>(D)));
-  uint32_t n = 0;
-  for (int t = blockIdx.x; t < total_items; t += gridDim.x) {
-    const DecItem it = dec_item(t, n_chunks, Hq, Hkv, sl, vlen, flags);
-    const bool row_vis = row_valid && flags[(size_t)it.s * Hq + it.g * rep + (row_valid ? gid : 0)];
+  uint32_t n = 0, ni = 0;
+  for (int t = blockIdx.x; t < total_items; t += gridDim.x, ++ni) {
+    DecItem it;
+    bool row_vis;
+    if constexpr (FUSED) {
+      const int slot = ni % NIT;
+      mbar_wait(smem_u32(&item_full[slot]), (ni / NIT) & 1);
+      const uint32_t mask = s_mask[slot];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&item_empty[slot]));
+      it = dec_item_mask(t, n_chunks, Hkv, sl, vlen, mask);
+      row_vis = row_valid && ((mask >> gid) & 1u);
+    } else {
+      it = dec_item(t, n_chunks, Hq, Hkv, sl, vlen, flags);
+      row_vis = row_valid && flags[(size_t)it.s * Hq + it.g * rep + (row_valid ? gid : 0)];
+    }
     // Q A-fragments, natural head-dim order: k-step ks covers d = 16 ks .. +15
     uint32_t qa[8][4];
     {
@@ -584,16 +704,20 @@ static int decode_step_impl(const void* q, const void* vision_k, const void* vis
   float* part_acc = part_ml + (size_t)batch * n_q_heads * nc * 2;
   int* degenerate = status ? reinterpret_cast<int*>(status)
                            : reinterpret_cast<int*>(part_acc + (size_t)batch * n_q_heads * nc * head_dim);
-  OMNI_CUDA_TRY(cudaMemsetAsync(degenerate, 0, sizeof(int), st));
-  dec::decode_flags_kernel<<<dim3(n_q_heads, batch), 32, 0, st>>>(static_cast<const __nv_bfloat16*>(q), k_lazy, k_act,
-                                                                   n_q_heads, n_kv_heads, tau, preserve_first_head,
-                                                                   flags_override, flags);
-  // K7 implementation: TMA-staged persistent kernel by default;
-  // OMNI_DECODE_IMPL=regs selects the register-staged kernel.
-  static const bool regs = [] {
+  // K7 implementation: the TMA-staged persistent kernel with the query
+  // classification fused in by default, then the split-K merge;
+  // OMNI_DECODE_IMPL=split classifies in a separate kernel first,
+  // OMNI_DECODE_IMPL=regs uses the register-staged partial kernel.
+  static const int impl = [] {
     const char* e = getenv("OMNI_DECODE_IMPL");
-    return e && strcmp(e, "regs") == 0;
+    return (e && strcmp(e, "regs") == 0) ? 2 : (e && strcmp(e, "split") == 0) ? 1 : 0;
   }();
+  const bool regs = impl == 2, fused = impl == 0;
+  OMNI_CUDA_TRY(cudaMemsetAsync(degenerate, 0, sizeof(int), st));
+  if (!fused)
+    dec::decode_flags_kernel<<<dim3(n_kv_heads, batch), 32, 0, st>>>(static_cast<const __nv_bfloat16*>(q), k_lazy,
+                                                                      k_act, n_q_heads, n_kv_heads, tau,
+                                                                      preserve_first_head, flags_override, flags);
   if (regs) {
     dec::decode_partial_kernel<<<dim3(nc, n_kv_heads, batch), 128, 0, st>>>(
         static_cast<const __nv_bfloat16*>(q), static_cast<const __nv_bfloat16*>(vision_k),
@@ -614,19 +738,20 @@ static int decode_step_impl(const void* q, const void* vision_k, const void* vis
       const int rc = omni_make_tmap_rows(&m[i], bases[i], rows[i], dec::D, 2, 64, dec::TK);
       if (rc) return rc;
     }
-    static bool attr = false;
-    if (!attr) {
-      OMNI_CUDA_TRY(cudaFuncSetAttribute(dec::decode_partial_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)dec::TSMEM));
-      attr = true;
+    auto kern = fused ? dec::decode_partial_tma_kernel<true> : dec::decode_partial_tma_kernel<false>;
+    static bool attr[2] = {false, false};
+    if (!attr[fused]) {
+      OMNI_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dec::TSMEM));
+      attr[fused] = true;
     }
     int dev = 0, sms = 148;
     OMNI_CUDA_TRY(cudaGetDevice(&dev));
     OMNI_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     const int items = nc * n_kv_heads * batch;
-    dec::decode_partial_tma_kernel<<<min(sms, items), (dec::NCW + 1) * 32, dec::TSMEM, st>>>(
-        m[0], m[1], m[2], m[3], m[4], m[5], static_cast<const __nv_bfloat16*>(q), vision_len, sl,
-        n_q_heads, n_kv_heads, vcap, acap, flags, part_ml, part_acc, nc, items);
+    const dec::FuseArgs fa{k_lazy, k_act, tau, preserve_first_head, flags_override, flags};
+    kern<<<min(sms, items), (dec::NCW + 1) * 32, dec::TSMEM, st>>>(
+        m[0], m[1], m[2], m[3], m[4], m[5], static_cast<const __nv_bfloat16*>(q), vision_len, sl, n_q_heads,
+        n_kv_heads, vcap, acap, flags, part_ml, part_acc, nc, items, fa);
   }
   dec::decode_combine_kernel<<<dim3(n_q_heads, batch), dec::D, 0, st>>>(part_ml, part_acc, nc, out, degenerate);
   int st_code = omni_launch_check();
