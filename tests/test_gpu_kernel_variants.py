@@ -54,15 +54,31 @@ for _g in range(K.shape[0]):
 """
 
 
+RAMP = r"""
+# keys drift along the group's mean query direction: the logits of a row rise
+# by ~5 (exp2 units) per 128-key tile across the sequence, so the running max
+# keeps growing past the 2^8 lazy-rescale threshold (many deferred rescales
+# in the fast path) while no single tile jumps by 2^64 (no fallback)
+for _g in range(K.shape[0]):
+    _u = Q[4 * _g:4 * _g + 4].reshape(-1, Q.shape[2]).mean(axis=0)
+    _u = _u / np.linalg.norm(_u)
+    _qu = float(np.mean(np.abs(Q[4 * _g:4 * _g + 4].reshape(-1, Q.shape[2]) @ _u)))
+    _alpha = 200.0 * np.sqrt(128.0) / (1.4426950408889634 * _qu)
+    K[_g] += (_alpha * np.arange(K.shape[1]) / K.shape[1])[:, None] * _u[None, :]
+"""
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("impl,poly,fast,jump", [("single", "0", "1", False), ("single", "4", "1", False),
                                                  ("single", "8", "1", False), ("single", "4", "0", False),
                                                  ("single", "4", "1", True), ("single", "4", "0", True),
+                                                 ("single", "6", "1", "ramp"), ("single", "6", "0", "ramp"),
                                                  ("pair", "0", "1", False), ("pair", "4", "1", False)])
 def test_forward_variant_matches_oracle(impl, poly, fast, jump):
     env = dict(os.environ, OMNI_FWD_IMPL=impl, OMNI_FWD_POLY=poly, OMNI_FWD_FAST=fast)
+    snippet = RAMP if jump == "ramp" else JUMP if jump else ""
     code = CODE.replace("Q, K, V = round_bf16(Q), round_bf16(K), round_bf16(V)",
-                        (JUMP if jump else "") + "Q, K, V = round_bf16(Q), round_bf16(K), round_bf16(V)")
+                        snippet + "Q, K, V = round_bf16(Q), round_bf16(K), round_bf16(V)")
     out = subprocess.run([sys.executable, "-c", code], cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stderr[-2000:]
     r = json.loads(out.stdout.strip().splitlines()[-1])
@@ -70,4 +86,4 @@ def test_forward_variant_matches_oracle(impl, poly, fast, jump):
     assert r["scaled_err"] <= 1.0, r  # |err| <= 0.02 + 0.02 |ref| (bf16 P, fp32 accumulation)
     if impl == "single" and fast == "1":
         # the fast kernel hands over to the safe re-run exactly when a logit jump exceeds 2^64
-        assert r["fallback"] == (1 if jump else 0), r
+        assert r["fallback"] == (1 if jump is True else 0), r
