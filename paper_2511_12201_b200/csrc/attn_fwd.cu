@@ -105,10 +105,18 @@ __device__ __forceinline__ void fwd_tile(int L, bool reuse, const CUtensorMap& t
                                          int* __restrict__ status) {
   extern __shared__ uint8_t smem_raw[];
   const int h = L % Hq;
-  const int tile = n_tiles_max - 1 - L / Hq;  // heaviest (latest rows) tiles first
+  // Heaviest (latest rows) tile pairs first, counted down from the largest
+  // active-row count over the heads (device-side: the grid is sized for N
+  // rows, so the tile pairs beyond every head's count come last and cost
+  // nothing, instead of opening the launch with waves of empty CTAs).
+  int cmax = 0;
+  for (int k = threadIdx.x & 31; k < Hq; k += 32) cmax = max(cmax, __ldg(counts + k));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) cmax = max(cmax, __shfl_xor_sync(0xffffffffu, cmax, o));
+  const int tile = (cmax + 2 * BM - 1) / (2 * BM) - 1 - L / Hq;
   const int cnt = __ldg(counts + h);
   const int row0 = tile * 2 * BM;
-  if (row0 >= cnt) return;
+  if (tile < 0 || row0 >= cnt) return;
 
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t sbase = smem_u32(smem);
