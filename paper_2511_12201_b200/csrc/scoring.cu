@@ -274,7 +274,7 @@ __global__ void __launch_bounds__(256) q_score_kernel(const T* __restrict__ Q, i
 // persistent double-buffered variant (one CTA of 16 warps per SM) measured
 // 343 us — the float64 instruction stream, not HBM, is the limit.
 constexpr int QSB_MAX_ROWS = 256;
-constexpr int QSB_CHUNKS = 4;
+constexpr int QSB_CHUNKS = 2;  // bulk-copy pieces per block (2: 0.194 ms vs 4: 0.198, 8: 0.207 at 64K)
 
 __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
