@@ -182,6 +182,13 @@ int omni_sparse_attn_bwd(const void* Q, const void* K_sel, const void* V_sel, co
                          const float* lse, const int32_t* rows, const int32_t* counts, const int32_t* selected,
                          const int32_t* sel_counts, int n_q_heads, int n_kv_heads, int seq_len, int head_dim, int cap,
                          float* dQ, float* dK_sel, float* dV_sel, float* dV_sink, void* workspace, void* stream);
+/* As omni_sparse_attn_bwd with dQ in dtype dq_dtype (OMNI_DTYPE_F32 or
+ * OMNI_DTYPE_BF16: the training dtype written directly by the dq kernel). */
+int omni_sparse_attn_bwd_ex(const void* Q, const void* K_sel, const void* V_sel, const void* O, const void* dO,
+                            const float* lse, const int32_t* rows, const int32_t* counts, const int32_t* selected,
+                            const int32_t* sel_counts, int n_q_heads, int n_kv_heads, int seq_len, int head_dim,
+                            int cap, int dq_dtype, void* dQ, float* dK_sel, float* dV_sel, float* dV_sink,
+                            void* workspace, void* stream);
 
 /* ---------------------------------------------------------------- K7
  * One slimmed decode step for a batch of sequences.

@@ -45,6 +45,8 @@ SIGNATURES = {
     "omni_sparse_attn_bwd_workspace": (_c_size, [_c_int, _c_int]),
     "omni_sparse_attn_bwd": (_c_int, [_p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _c_int, _c_int, _c_int, _c_int,
                                       _c_int, _p, _p, _p, _p, _p, _p]),
+    "omni_sparse_attn_bwd_ex": (_c_int, [_p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _c_int, _c_int, _c_int, _c_int,
+                                         _c_int, _c_int, _p, _p, _p, _p, _p, _p]),
     "omni_decode_workspace": (_c_size, [_c_int, _c_int, _c_int, _c_int, _c_int, _c_int]),
     "omni_decode_step": (_c_int, [_p, _p, _p, _p, _p, _p, _c_int, _p, _p, _c_int, _p, _p, _c_int, _c_int,
                                   _c_int, _c_int, _c_int, _c_int, _c_double, _c_int, _p, _p, _p, _p, _p]),

@@ -47,15 +47,16 @@ class SparseAttentionFn(torch.autograd.Function):
         plan = ctx.plan
         hkv = K_sel.shape[0]
         n = Qb.shape[1]
+        qd, kd, vd = ctx.dtypes
         dQ, dKs, dVs, dVsink = ops.sparse_attn_bwd(Qb, K_sel, V_sel, O, dO.to(torch.bfloat16).contiguous(), lse,
-                                                   plan.rows, plan.counts, plan.selected, plan.sel_counts)
+                                                   plan.rows, plan.counts, plan.selected, plan.sel_counts,
+                                                   dq_dtype=torch.bfloat16 if qd == torch.bfloat16 else torch.float32)
         # compacted key gradients back to their original positions (device
         # counts: no host round trip)
         dK = ops.scatter_rows(dKs, plan.selected, plan.sel_counts,
                               torch.zeros(hkv, n, Qb.shape[2], device=Qb.device, dtype=torch.float32))
         dV = ops.scatter_rows(dVs, plan.selected, plan.sel_counts, torch.zeros_like(dK))
         dV[:, plan.sink_index] += dVsink
-        qd, kd, vd = ctx.dtypes
         return dQ.to(qd), dK.to(kd), dV.to(vd), None
 
 

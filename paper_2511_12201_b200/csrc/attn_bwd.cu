@@ -137,7 +137,7 @@ dq_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
           const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
           const int32_t* __restrict__ rows, const int32_t* __restrict__ counts, const float* __restrict__ lse2c,
           const float* __restrict__ Dc, const int32_t* __restrict__ visc, int Hq, int rep, int N, int cap, int capq,
-          int n_tiles, float* __restrict__ dQ) {
+          int n_tiles, void* __restrict__ dQ, int dq_bf16) {
   using namespace dq;
   extern __shared__ uint8_t smem_raw[];
   const int L = blockIdx.x;
@@ -325,16 +325,26 @@ dq_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
       tc_fence_after();
       const float scale = static_cast<float>(1.0 / sqrt(static_cast<double>(D)));
       const int pos = valid ? __ldg(rows + (size_t)h * N + r0 + i) : 0;
-      float4* dst = reinterpret_cast<float4*>(dQ + ((size_t)h * N + pos) * D + cb);
       uint32_t o[32];
       __syncwarp();
       tmem_ld32(tl + COL_DQ + cb, o);
       tmem_wait_ld();
       if (valid) {
+        if (dq_bf16) {  // the training dtype directly: no fp32 round trip through HBM
+          uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(dQ) + ((size_t)h * N + pos) * D + cb);
 #pragma unroll
-        for (int q = 0; q < 8; ++q)
-          dst[q] = make_float4(__uint_as_float(o[4 * q]) * scale, __uint_as_float(o[4 * q + 1]) * scale,
-                               __uint_as_float(o[4 * q + 2]) * scale, __uint_as_float(o[4 * q + 3]) * scale);
+          for (int q = 0; q < 4; ++q) {
+            const float* f = reinterpret_cast<const float*>(o + 8 * q);
+            dst[q] = make_uint4(pack_bf16x2(f[0] * scale, f[1] * scale), pack_bf16x2(f[2] * scale, f[3] * scale),
+                                pack_bf16x2(f[4] * scale, f[5] * scale), pack_bf16x2(f[6] * scale, f[7] * scale));
+          }
+        } else {
+          float4* dst = reinterpret_cast<float4*>(static_cast<float*>(dQ) + ((size_t)h * N + pos) * D + cb);
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            dst[q] = make_float4(__uint_as_float(o[4 * q]) * scale, __uint_as_float(o[4 * q + 1]) * scale,
+                                 __uint_as_float(o[4 * q + 2]) * scale, __uint_as_float(o[4 * q + 3]) * scale);
+        }
       }
     }
   }
@@ -997,11 +1007,12 @@ extern "C" size_t omni_sparse_attn_bwd_workspace(int n_q_heads, int seq_len) {
   return rows * bwd::D * 2 * 2 + rows * 4 * 3 + 1024;
 }
 
-extern "C" int omni_sparse_attn_bwd(const void* Q, const void* K_sel, const void* V_sel, const void* O, const void* dO,
-                                    const float* lse, const int32_t* rows, const int32_t* counts,
-                                    const int32_t* selected, const int32_t* sel_counts, int n_q_heads, int n_kv_heads,
-                                    int seq_len, int head_dim, int cap, float* dQ, float* dK_sel, float* dV_sel,
-                                    float* dV_sink, void* workspace, void* stream) {
+extern "C" int omni_sparse_attn_bwd_ex(const void* Q, const void* K_sel, const void* V_sel, const void* O,
+                                       const void* dO, const float* lse, const int32_t* rows, const int32_t* counts,
+                                       const int32_t* selected, const int32_t* sel_counts, int n_q_heads,
+                                       int n_kv_heads, int seq_len, int head_dim, int cap, int dq_dtype, void* dQ,
+                                       float* dK_sel, float* dV_sel, float* dV_sink, void* workspace, void* stream) {
+  OMNI_CHECK(dq_dtype == OMNI_DTYPE_F32 || dq_dtype == OMNI_DTYPE_BF16, OMNI_E_PARAM, "dQ must be f32 or bf16");
   OMNI_CHECK(head_dim == 128, OMNI_E_SHAPE, "sparse attention backward requires head_dim == 128");
   OMNI_CHECK(n_kv_heads >= 1 && n_q_heads % n_kv_heads == 0, OMNI_E_SHAPE, "n_q_heads must be a multiple of n_kv_heads");
   OMNI_CHECK(n_q_heads / n_kv_heads <= 16, OMNI_E_SHAPE, "at most 16 Q heads per KV group");
@@ -1016,7 +1027,8 @@ extern "C" int omni_sparse_attn_bwd(const void* Q, const void* K_sel, const void
   float* lse2c = reinterpret_cast<float*>(dOc + crow * bwd::D);
   float* Dc = lse2c + crow;
   int32_t* visc = reinterpret_cast<int32_t*>(Dc + crow);
-  OMNI_CUDA_TRY(cudaMemsetAsync(dQ, 0, sizeof(float) * (size_t)n_q_heads * seq_len * head_dim, st));
+  const size_t dq_esz = dq_dtype == OMNI_DTYPE_BF16 ? 2 : 4;
+  OMNI_CUDA_TRY(cudaMemsetAsync(dQ, 0, dq_esz * (size_t)n_q_heads * seq_len * head_dim, st));
   OMNI_CUDA_TRY(cudaMemsetAsync(dK_sel, 0, sizeof(float) * (size_t)n_kv_heads * cap * head_dim, st));
   OMNI_CUDA_TRY(cudaMemsetAsync(dV_sel, 0, sizeof(float) * (size_t)n_kv_heads * cap * head_dim, st));
   OMNI_CUDA_TRY(cudaMemsetAsync(dV_sink, 0, sizeof(float) * (size_t)n_kv_heads * head_dim, st));
@@ -1047,7 +1059,7 @@ extern "C" int omni_sparse_attn_bwd(const void* Q, const void* K_sel, const void
   }();
   (dq_probe == 1 ? bwd::dq_kernel<1> : bwd::dq_kernel<0>)<<<n_tiles * n_q_heads, 576, bwd::dq::SMEM, st>>>(tq128, tdo128, tk, tv, rows, counts, lse2c, Dc,
                                                                     visc, n_q_heads, rep, seq_len, cap, capq, n_tiles,
-                                                                    dQ);
+                                                                    dQ, dq_dtype == OMNI_DTYPE_BF16 ? 1 : 0);
   if ((rc = omni_launch_check())) return rc;
   // dkv implementation: TMEM-resident P^T / dS^T kernel by default;
   // OMNI_BWD_DKV=v1 selects the shared-memory P^T kernel.
@@ -1087,4 +1099,14 @@ extern "C" int omni_debug_bwd_trace(unsigned long long* host8) {
   unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   OMNI_CUDA_TRY(cudaMemcpyToSymbol(bwd::g_bwd_trace, z, sizeof(z)));
   return OMNI_OK;
+}
+
+extern "C" int omni_sparse_attn_bwd(const void* Q, const void* K_sel, const void* V_sel, const void* O, const void* dO,
+                                    const float* lse, const int32_t* rows, const int32_t* counts,
+                                    const int32_t* selected, const int32_t* sel_counts, int n_q_heads, int n_kv_heads,
+                                    int seq_len, int head_dim, int cap, float* dQ, float* dK_sel, float* dV_sel,
+                                    float* dV_sink, void* workspace, void* stream) {
+  return omni_sparse_attn_bwd_ex(Q, K_sel, V_sel, O, dO, lse, rows, counts, selected, sel_counts, n_q_heads,
+                                 n_kv_heads, seq_len, head_dim, cap, OMNI_DTYPE_F32, dQ, dK_sel, dV_sel, dV_sink,
+                                 workspace, stream);
 }

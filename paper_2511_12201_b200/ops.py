@@ -220,19 +220,23 @@ def _status_word(device) -> torch.Tensor:
     return _STATUS[key]
 
 
-def sparse_attn_bwd(Q, K_sel, V_sel, O, dO, lse, rows, counts, selected, sel_counts):
+def sparse_attn_bwd(Q, K_sel, V_sel, O, dO, lse, rows, counts, selected, sel_counts, dq_dtype=torch.float32):
     """Backward of K4 over the compacted keys; returns (dQ, dK_sel, dV_sel,
-    dV_sink) in fp32."""
+    dV_sink): dK / dV in fp32 (reduced over the group's Q heads), dQ in
+    ``dq_dtype`` (fp32 or bf16, written directly by the dq kernel)."""
     hq, n, d = Q.shape
     hkv, cap, _ = K_sel.shape
     f32 = dict(device=Q.device, dtype=torch.float32)
-    dQ = torch.empty(hq, n, d, **f32)
+    if dq_dtype not in (torch.float32, torch.bfloat16):
+        raise ParameterError("dQ dtype must be float32 or bfloat16")
+    dQ = torch.empty(hq, n, d, device=Q.device, dtype=dq_dtype)
     dK = torch.empty(hkv, cap, d, **f32)
     dV = torch.empty(hkv, cap, d, **f32)
     dVs = torch.empty(hkv, d, **f32)
     ws = torch.empty(max(1, _lib.size("omni_sparse_attn_bwd_workspace", hq, n)), device=Q.device, dtype=torch.uint8)
-    _lib.call("omni_sparse_attn_bwd", _p(Q), _p(K_sel), _p(V_sel), _p(O), _p(dO), _p(lse), _p(rows), _p(counts),
-              _p(selected), _p(sel_counts), hq, hkv, n, d, cap, _p(dQ), _p(dK), _p(dV), _p(dVs), _p(ws), _stream())
+    _lib.call("omni_sparse_attn_bwd_ex", _p(Q), _p(K_sel), _p(V_sel), _p(O), _p(dO), _p(lse), _p(rows), _p(counts),
+              _p(selected), _p(sel_counts), hq, hkv, n, d, cap, _dtype(dQ), _p(dQ), _p(dK), _p(dV), _p(dVs), _p(ws),
+              _stream())
     return dQ, dK, dV, dVs
 
 
