@@ -180,7 +180,11 @@ __global__ void __launch_bounds__(256) probe_mass_fused_kernel(const double* __r
       for (int J = lane; J <= I; J += 32) mx = fmax(mx, S[ii * nb + J]);
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-      for (int J = lane; J <= I; J += 32) sum += exp(S[ii * nb + J] - mx);
+      for (int J = lane; J <= I; J += 32) {  // keep exp(S - max) for the column pass
+        const double e = exp(S[ii * nb + J] - mx);
+        S[ii * nb + J] = e;
+        sum += e;
+      }
       sum = warp_sum(sum);
     }
     if (lane == 0) { s_m[ii] = mx; s_l[ii] = sum; }
@@ -192,7 +196,7 @@ __global__ void __launch_bounds__(256) probe_mass_fused_kernel(const double* __r
     double t = 0.0;
     for (int ii = max(0, J - I0); ii < PF_ROWS; ++ii) {
       const int I = I0 + ii;
-      if (I < nb) t += exp(S[ii * nb + J] - s_m[ii]) / s_l[ii];
+      if (I < nb) t += S[ii * nb + J] / s_l[ii];
     }
     out[J] = t;
   }
