@@ -142,6 +142,14 @@ int omni_gather_rows(const void* src, int dtype, int n_groups, int src_rows, int
                      int idx_stride, const int32_t* counts, int count_const, void* dst, int dst_rows, int pad_rows,
                      void* stream);
 
+/* Cache slimming for one sequence (build_cache, decode.py:82-108; the
+ * omni_slim_cache of SURVEY §8b): vision_k/v [Hkv, vcap, d] = K/V rows
+ * vision_selected[g, :budget] (ascending, inside the vision span), rows
+ * [budget, vcap) zero. Errors: INTEGRITY when budget is outside [1, vcap]. */
+int omni_slim_cache(const void* K, const void* V, int dtype, int n_kv_heads, int seq_len, int head_dim,
+                    const int32_t* vision_selected, int sel_stride, int budget, int vcap, void* vision_k,
+                    void* vision_v, void* stream);
+
 /* Inverse of omni_gather_rows: dst[g, idx[g, r]] = src[g, r] for
  * r < counts[g] (device i32 [G]); other dst rows are untouched. Used to put
  * compacted key gradients back at their original positions. */
@@ -226,6 +234,13 @@ int omni_decode_step_varlen(const void* q, const void* vision_k, const void* vis
                             int head_dim, int vcap, int acap, double tau, int preserve_first_head,
                             const uint8_t* flags_override, uint8_t* flags, float* out, void* workspace,
                             int32_t* status, void* stream);
+
+/* omni_decode (SURVEY §8b's name for K7): identical to omni_decode_step.   */
+int omni_decode(const void* q, const void* vision_k, const void* vision_v, const int32_t* vision_len,
+                const void* text_k, const void* text_v, int n_text, const void* answer_k, const void* answer_v,
+                int n_answer, const double* k_lazy, const double* k_act, int batch, int n_q_heads, int n_kv_heads,
+                int head_dim, int vcap, int acap, double tau, int preserve_first_head,
+                const uint8_t* flags_override, uint8_t* flags, float* out, void* workspace, void* stream);
 
 #ifdef __cplusplus
 }

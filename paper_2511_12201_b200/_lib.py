@@ -50,6 +50,9 @@ SIGNATURES = {
     "omni_decode_workspace": (_c_size, [_c_int, _c_int, _c_int, _c_int, _c_int, _c_int]),
     "omni_decode_step": (_c_int, [_p, _p, _p, _p, _p, _p, _c_int, _p, _p, _c_int, _p, _p, _c_int, _c_int,
                                   _c_int, _c_int, _c_int, _c_int, _c_double, _c_int, _p, _p, _p, _p, _p]),
+    "omni_decode": (_c_int, [_p, _p, _p, _p, _p, _p, _c_int, _p, _p, _c_int, _p, _p, _c_int, _c_int,
+                             _c_int, _c_int, _c_int, _c_int, _c_double, _c_int, _p, _p, _p, _p, _p]),
+    "omni_slim_cache": (_c_int, [_p, _p, _c_int, _c_int, _c_int, _c_int, _p, _c_int, _c_int, _c_int, _p, _p, _p]),
     "omni_decode_step_varlen": (_c_int, [_p, _p, _p, _p, _p, _p, _p, _c_int, _p, _p, _p, _p, _p, _c_int, _c_int,
                                          _c_int, _c_int, _c_int, _c_int, _c_double, _c_int, _p, _p, _p, _p, _p,
                                          _p]),

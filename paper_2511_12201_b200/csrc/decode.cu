@@ -793,3 +793,16 @@ extern "C" int omni_decode_step_varlen(const void* q, const void* vision_k, cons
                           batch, n_q_heads, n_kv_heads, head_dim, vcap, acap, tau, preserve_first_head,
                           flags_override, flags, out, workspace, status, stream);
 }
+
+// SURVEY §8b's minimum export set names the decode entry point omni_decode;
+// it is omni_decode_step.
+extern "C" int omni_decode(const void* q, const void* vision_k, const void* vision_v, const int32_t* vision_len,
+                           const void* text_k, const void* text_v, int n_text, const void* answer_k,
+                           const void* answer_v, int n_answer, const double* k_lazy, const double* k_act, int batch,
+                           int n_q_heads, int n_kv_heads, int head_dim, int vcap, int acap, double tau,
+                           int preserve_first_head, const uint8_t* flags_override, uint8_t* flags, float* out,
+                           void* workspace, void* stream) {
+  return omni_decode_step(q, vision_k, vision_v, vision_len, text_k, text_v, n_text, answer_k, answer_v, n_answer,
+                          k_lazy, k_act, batch, n_q_heads, n_kv_heads, head_dim, vcap, acap, tau, preserve_first_head,
+                          flags_override, flags, out, workspace, stream);
+}

@@ -636,3 +636,19 @@ extern "C" int omni_scatter_rows(const void* src, int dtype, int n_groups, int s
       dst_rows);
   return omni_launch_check();
 }
+
+// SURVEY §8b's minimum export set names the cache slimming entry point
+// omni_slim_cache: build_cache's pruning + regrouping (decode.py:92-107) of one
+// sequence — the budget selected vision rows of K and V per KV group into the
+// slim cache segments [Hkv, vcap, d], rows past the budget zero-filled (the
+// TMA-staged decode reads whole 64-row tiles).
+extern "C" int omni_slim_cache(const void* K, const void* V, int dtype, int n_kv_heads, int seq_len, int head_dim,
+                               const int32_t* vision_selected, int sel_stride, int budget, int vcap, void* vision_k,
+                               void* vision_v, void* stream) {
+  OMNI_CHECK(budget >= 1 && budget <= vcap, OMNI_E_INTEGRITY, "budget outside [1, vision capacity]");
+  int rc = omni_gather_rows(K, dtype, n_kv_heads, seq_len, head_dim, vision_selected, sel_stride, nullptr, budget,
+                            vision_k, vcap, vcap, stream);
+  if (rc) return rc;
+  return omni_gather_rows(V, dtype, n_kv_heads, seq_len, head_dim, vision_selected, sel_stride, nullptr, budget,
+                          vision_v, vcap, vcap, stream);
+}

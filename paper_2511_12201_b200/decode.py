@@ -121,8 +121,7 @@ def build_cache(K: torch.Tensor, V: torch.Tensor, vision_selected: torch.Tensor,
     Vb = V if V.dtype == torch.bfloat16 else V.to(torch.bfloat16)
     # rows [budget, vcap) are zero-filled: the TMA-staged decode kernel reads
     # whole 64-key tiles and masks keys past the budget (P = 0 needs finite V)
-    vk = ops.gather_rows(Kb, vision_selected, budget, vcap, vcap).unsqueeze(0)
-    vv = ops.gather_rows(Vb, vision_selected, budget, vcap, vcap).unsqueeze(0)
+    vk, vv = (t.unsqueeze(0) for t in ops.slim_cache(Kb, Vb, vision_selected, budget, vcap))
     idx = torch.zeros(1, hkv, vcap, dtype=torch.int32, device=K.device)
     idx[0, :, :budget] = vision_selected[:, :budget]
     tk = Kb[:, n_vision:n_vision + n_text].contiguous().unsqueeze(0)

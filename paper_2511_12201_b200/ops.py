@@ -178,6 +178,20 @@ def gather_rows(src: torch.Tensor, idx: torch.Tensor, counts: torch.Tensor | int
     return out
 
 
+def slim_cache(K: torch.Tensor, V: torch.Tensor, vision_selected: torch.Tensor, budget: int, vcap: int):
+    """build_cache's pruning + regrouping (decode.py:92-107): the budget
+    selected vision rows of every KV group, [Hkv, vcap, d], rows past the
+    budget zero (omni_slim_cache)."""
+    _cuda3(K, "K")
+    _cuda3(V, "V")
+    hkv, n, d = K.shape
+    vk = torch.empty(hkv, vcap, d, device=K.device, dtype=K.dtype)
+    vv = torch.empty_like(vk)
+    _lib.call("omni_slim_cache", _p(K), _p(V), _dtype(K), hkv, n, d, _p(vision_selected), vision_selected.shape[-1],
+              int(budget), int(vcap), _p(vk), _p(vv), _stream())
+    return vk, vv
+
+
 def scatter_rows(src: torch.Tensor, idx: torch.Tensor, counts: torch.Tensor, out: torch.Tensor) -> torch.Tensor:
     """out[g, idx[g, r]] = src[g, r] for r < counts[g] (inverse of gather_rows)."""
     _cuda3(src, "src")
