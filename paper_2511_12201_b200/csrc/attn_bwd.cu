@@ -647,7 +647,10 @@ constexpr int NI = 4;                                                           
 constexpr uint32_t OFF_INFO = 6 * TILE;                                           // [NI][3][128]
 constexpr uint32_t OFF_BAR = OFF_INFO + NI * 3 * BR * 4;
 // B_TF: S^T(k) ready; B_SF: dP^T(k) ready; B_SE: S^T(k) read by every gradient thread
-enum { B_KV = 0, B_QF = 1, B_QE = 3, B_IF = 5, B_IE = 5 + NI, B_SF = 5 + 2 * NI, B_SE, B_PF, B_PE, B_TF, B_N };
+// Q and dO have separate rings (B_QF/B_QE, B_DF/B_DE): dK(k), the last use
+// of Q(k), runs before dV(k), so the Q stage the next S^T needs frees early.
+enum { B_KV = 0, B_QF = 1, B_QE = 3, B_IF = 5, B_IE = 5 + NI, B_SF = 5 + 2 * NI, B_SE, B_PF, B_PE, B_TF, B_DF,
+       B_DE = B_DF + 2, B_N = B_DE + 2 };
 constexpr uint32_t OFF_TMEM = OFF_BAR + 8 * B_N;
 constexpr uint32_t SMEM = OFF_TMEM + 16 + 1024;
 constexpr uint32_t COL_S = 0, COL_DP = 128, COL_DV = 256, COL_DK = 384;
@@ -703,6 +706,8 @@ dkv2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
     for (int s = 0; s < 2; ++s) {
       mbar_init(B(B_QF + s), 1);
       mbar_init(B(B_QE + s), 1);
+      mbar_init(B(B_DF + s), 1);
+      mbar_init(B(B_DE + s), 1);
     }
     for (int s = 0; s < NI; ++s) {
       mbar_init(B(B_IF + s), 64);
@@ -737,11 +742,13 @@ dkv2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
         const int s = k & 1;
         const int row = h * capq + (first + k) * BR;
         if (k >= 2) mbar_wait(B(B_QE + s), ((k >> 1) - 1) & 1);
-        mbar_expect_tx(B(B_QF + s), 2 * TILE);
+        mbar_expect_tx(B(B_QF + s), TILE);
         tma_load_2d(sb + OFF_Q + s * TILE, &tm_q, B(B_QF + s), 0, row);
         tma_load_2d(sb + OFF_Q + s * TILE + ATOM, &tm_q, B(B_QF + s), 64, row);
-        tma_load_2d(sb + OFF_DO + s * TILE, &tm_do, B(B_QF + s), 0, row);
-        tma_load_2d(sb + OFF_DO + s * TILE + ATOM, &tm_do, B(B_QF + s), 64, row);
+        if (k >= 2) mbar_wait(B(B_DE + s), ((k >> 1) - 1) & 1);
+        mbar_expect_tx(B(B_DF + s), TILE);
+        tma_load_2d(sb + OFF_DO + s * TILE, &tm_do, B(B_DF + s), 0, row);
+        tma_load_2d(sb + OFF_DO + s * TILE + ATOM, &tm_do, B(B_DF + s), 64, row);
       }
     }
   } else if (warp == 1) {
@@ -768,6 +775,8 @@ dkv2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
       };
       auto issue_dpt = [&](int k) {  // dP^T(k) = V dO(k)^T -> COL_DP
         const int s = k & 1;
+        mbar_wait(B(B_DF + s), (k >> 1) & 1);
+        tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
           const uint32_t off = ((kk >> 2) * ATOM + (kk & 3) * 32) >> 4;
@@ -794,24 +803,25 @@ dkv2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
         }
         tc_fence_after();
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {  // K = 128 rows, 16 per MMA
-          const uint32_t ac = COL_DP + 32u * (kk >> 1) + 8u * (kk & 1);
-          umma_bf16_ts_ws(tmem + COL_DV, tmem + ac, ddom0 + ((s * TILE + kk * 2048) >> 4), id_acc,
-                          (k > 0 || kk > 0) ? 1u : 0u);
-        }
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
+        for (int kk = 0; kk < 8; ++kk) {  // dK += dS^T Q, K = 128 rows, 16 per MMA
           const uint32_t ac = COL_DP + 32u * (kk >> 1) + 16u + 8u * (kk & 1);
           umma_bf16_ts_ws(tmem + COL_DK, tmem + ac, dqm0 + ((s * TILE + kk * 2048) >> 4), id_acc,
                           (k > 0 || kk > 0) ? 1u : 0u);
         }
-        umma_commit_ws(B(B_QE + s));
+        umma_commit_ws(B(B_QE + s));  // Q(k) free: the Q(k + 2) load starts under dV(k)
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {  // dV += P^T dO
+          const uint32_t ac = COL_DP + 32u * (kk >> 1) + 8u * (kk & 1);
+          umma_bf16_ts_ws(tmem + COL_DV, tmem + ac, ddom0 + ((s * TILE + kk * 2048) >> 4), id_acc,
+                          (k > 0 || kk > 0) ? 1u : 0u);
+        }
+        umma_commit_ws(B(B_DE + s));
         umma_commit_ws(B(B_PE));
         if (k + 1 < total) issue_dpt(k + 1);  // after dV / dK(k): they read the dP^T region
       }
       if constexpr (PROBE == 3) {
         if (lane == 0) {
-          atomicAdd(&g_bwd_trace[4], (unsigned long long)tw_se);
+          (void)tw_se;
           (void)tw_pf;
           atomicAdd(&g_bwd_trace[3], (unsigned long long)tw_qf);  // (overrides the gradient st slot)
           atomicAdd(&g_bwd_trace[7], (unsigned long long)total);
@@ -915,7 +925,9 @@ dkv2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
       };
       if (full) pmath(std::true_type{}); else pmath(std::false_type{});
       // phase 2: dS^T = P^T (dP^T - D) with the bf16 P^T (the values dV uses)
+      const uint32_t cs0 = clock();
       mbar_wait(B(B_SF), k & 1);
+      const uint32_t cs1 = clock();
       tc_fence_after();
       uint32_t dp[32];
       __syncwarp();
@@ -946,15 +958,16 @@ dkv2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
       mbar_arrive(B(B_PF));
       if constexpr (PROBE == 3) {
         const uint32_t c4 = clock();
-        tg[0] += c1 - c0;
-        tg[1] += c2c - c1;
-        tg[2] += c3 - c2i;
-        tg[3] += c4 - c3;
+        tg[0] += c1 - c0;      // wait S^T
+        tg[1] += cs0 - c2c;    // ld S^T + info + P^T phase
+        tg[2] += cs1 - cs0;    // wait dP^T
+        tg[3] += c4 - cs1;     // ld dP^T, dS^T, stores, release
       }
     }
     if constexpr (PROBE == 3) {
       if (lane == 0) {
         for (int q = 0; q < 3; ++q) atomicAdd(&g_bwd_trace[q], (unsigned long long)tg[q]);
+        atomicAdd(&g_bwd_trace[4], (unsigned long long)tg[3]);  // (overrides the MMA SE wait slot)
         atomicAdd(&g_bwd_trace[6], (unsigned long long)total);
         atomicAdd(&g_bwd_trace[5], (unsigned long long)tg[4]);  // (overrides the MMA PF wait slot)
       }

@@ -21,6 +21,6 @@ lib.omni_debug_bwd_trace(buf)
 O = SparseAttentionFn.apply(Q, K, V, plan); O.backward(dO); torch.cuda.synchronize()
 lib.omni_debug_bwd_trace(buf)
 v = list(buf)
-g = {nm: v[k] / v[6] for k, nm in enumerate(["wait_SF", "ld", "compute"])}; g["mma_wait_QF"] = v[3] / v[7]
-m = {"mma_wait_SE": v[4] / v[7], "grad_wait_IF": v[5] / v[6]}
+g = {nm: v[k] / v[6] for k, nm in enumerate(["wait_ST", "P_phase", "wait_dPT"])}; g["dS_phase"] = v[4] / v[6]; g["mma_wait_QF"] = v[3] / v[7]
+m = {"grad_wait_IF": v[5] / v[6]}
 print(json.dumps({"grad_cycles_per_step": g, "mma_cycles_per_step": m, "steps": v[7]}))
