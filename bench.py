@@ -413,9 +413,17 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # OMNI_BENCH_SHARED_GPU=1 (testing the N > 1 code path on a one-GPU box):
+    # every rank on device 0, gloo instead of NCCL
+    shared = os.environ.get("OMNI_BENCH_SHARED_GPU") == "1"
+    if shared:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     ops.device_check()
     hbm_peak, tc_peak, tc_sus, peak_src = peaks()
     n, nv = args.seq, args.seq - N_TEXT
@@ -466,6 +474,8 @@ def run_ours(args):
                        "parallelism": f"head-sharded x{world}" if world > 1 else "single GPU",
                        "l2": "inputs larger than L2 (Q alone 470 MB at 64K); no flush"}}
     line["clocks"] = clk.summary()
+    if world > 1:
+        multi_rank_sections(args, line, step, res, plan, Ql, Kl, Vl, O, nv, cfg, world, tc_peak, peak_src)
     if rank != 0:
         if world > 1:
             dist.barrier()
@@ -644,6 +654,76 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def work_flops_shard(res, plan, d: int = D) -> float:
+    """work_flops for one rank's Q heads (rows / counts local, selection global)."""
+    import torch
+
+    rep = plan.n_q_heads // plan.n_kv_heads
+    counts = res.counts.cpu().tolist()
+    b = res.selection.info[4:].cpu().tolist()
+    total = 0
+    for hl in range(res.rows.shape[0]):
+        g = (plan.q_start + hl) // rep
+        sel = res.selection.selected[g, : b[g]].contiguous()
+        rows = res.rows[hl, : counts[hl]].contiguous()
+        total += int(torch.searchsorted(sel, rows, right=True).sum())
+    return 4.0 * d * total
+
+
+def multi_rank_sections(args, line, step, res, plan, Ql, Kl, Vl, O, nv, cfg, world, tc_peak, peak_src):
+    """N > 1 (every rank, same collective order): the K4 roofline over the
+    shards (sum of the ranks' algorithmic FLOPs / the slowest rank's K4 time,
+    per GPU), this rank's launch count, and the end-to-end metric through host
+    buffers (each rank copies its shard of Q/K/V in and its O rows out)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2511_12201_b200 import ops
+    from paper_2511_12201_b200.parallel import sparse_prefill_sharded
+
+    sel_loc = res.selection.selected[plan.g_start:plan.g_stop]
+    cnt_loc = res.selection.info[4 + plan.g_start: 4 + plan.g_stop]
+    fa = lambda: ops.sparse_attn_fwd(Ql, res.K_sel, res.V_sel, Vl, res.rows, res.counts, sel_loc, cnt_loc,
+                                     cfg.sink_index, O, res.lse)
+    fa_ms = time_cuda(fa, args.steps, 2)
+    flops = work_flops_shard(res, plan)
+    t = torch.tensor([fa_ms], device="cuda")
+    f = torch.tensor([flops], device="cuda", dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dist.all_reduce(f, op=dist.ReduceOp.SUM)
+    achieved = float(f) / (float(t) / 1e3) / 1e12 / world
+    line["roofline"] = {"bound": "tensor", "kernel": "omni sparse_fwd_kernel (K4), per GPU over the shards",
+                        "achieved": achieved, "peak": tc_peak, "unit": "TFLOP/s", "frac": achieved / tc_peak,
+                        "traffic": None, "peak_source": f"{peak_src} bf16 burst (MEASURED_PEAKS.json)",
+                        "launch_ms_max_over_ranks": float(t)}
+    n_ours, n_all, names = count_launches(step)
+    line["gpu_launches"] = n_ours * args.steps
+    line["gpu_launches_per_step"] = {"ours_per_rank": n_ours, "all_per_rank": n_all, "kernels": names}
+    if not args.no_e2e:
+        hQ, hK, hV = (x.cpu().pin_memory() for x in (Ql, Kl, Vl))
+        hO = torch.empty(O.shape, dtype=torch.bfloat16).pin_memory()
+
+        def e2e():
+            Ql.copy_(hQ, non_blocking=True)
+            Kl.copy_(hK, non_blocking=True)
+            Vl.copy_(hV, non_blocking=True)
+            sparse_prefill_sharded(Ql, Kl, Vl, plan, nv, world, cfg, out=O)
+            hO.copy_(O, non_blocking=True)
+
+        dist.barrier()
+        e_ms = time_cuda(e2e, max(3, args.steps // 2), 1)
+        te = torch.tensor([e_ms], device="cuda")
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        n = Ql.shape[1]
+        nb = torch.tensor([sum(x.numel() * x.element_size() for x in (hQ, hK, hV)), hO.numel() * hO.element_size()],
+                          device="cuda", dtype=torch.float64)
+        dist.all_reduce(nb, op=dist.ReduceOp.SUM)
+        line["e2e"] = {"value": n / (float(te) / 1e3), "unit": "tok/s", "ms_per_step": float(te),
+                       "h2d_bytes_per_step": int(nb[0]), "d2h_bytes_per_step": int(nb[1]),
+                       "api": "parallel.sparse_prefill_sharded per rank: pinned host shard in, host O rows out "
+                              "(time: max over ranks; bytes: summed over ranks)"}
 
 
 def run_reference(args):
