@@ -235,6 +235,13 @@ int omni_decode_step_varlen(const void* q, const void* vision_k, const void* vis
                             const uint8_t* flags_override, uint8_t* flags, float* out, void* workspace,
                             int32_t* status, void* stream);
 
+/* append_answer (decode.py:111-121) for a batch in one launch: bf16 k/v_rows
+ * [B, Hkv, d] go to answer_k/v [B, Hkv, acap, d] at row answer_len[s]
+ * (device i32 [B], incremented; ragged batches) or n_answer (answer_len
+ * NULL). The caller guarantees the row is below acap.                      */
+int omni_append_answer(const void* k_rows, const void* v_rows, void* answer_k, void* answer_v, int batch,
+                       int n_kv_heads, int head_dim, int acap, int n_answer, int32_t* answer_len, void* stream);
+
 /* omni_decode (SURVEY §8b's name for K7): identical to omni_decode_step.   */
 int omni_decode(const void* q, const void* vision_k, const void* vision_v, const int32_t* vision_len,
                 const void* text_k, const void* text_v, int n_text, const void* answer_k, const void* answer_v,

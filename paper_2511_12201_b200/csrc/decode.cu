@@ -806,3 +806,36 @@ extern "C" int omni_decode(const void* q, const void* vision_k, const void* visi
                           k_lazy, k_act, batch, n_q_heads, n_kv_heads, head_dim, vcap, acap, tau, preserve_first_head,
                           flags_override, flags, out, workspace, stream);
 }
+
+// append_answer (decode.py:111-121) for a batch, one launch: the new K / V row
+// of every (sequence, KV group) goes to answer row pos_s = answer_len[s]
+// (ragged batches; incremented here) or n_answer (answer_len NULL). One CTA
+// per sequence, so the position is read before it is advanced.
+__global__ void append_answer_kernel(const uint4* __restrict__ k_rows, const uint4* __restrict__ v_rows,
+                                     uint4* __restrict__ ak, uint4* __restrict__ av, int Hkv, int acap, int n_answer,
+                                     int32_t* __restrict__ answer_len) {
+  constexpr int RV = dec::D * 2 / 16;  // uint4 per bf16 row
+  const int s = blockIdx.x;
+  const int pos = answer_len ? answer_len[s] : n_answer;
+  for (int e = threadIdx.x; e < Hkv * RV; e += blockDim.x) {
+    const int g = e / RV, c = e % RV;
+    const size_t src = ((size_t)s * Hkv + g) * RV + c;
+    const size_t dst = (((size_t)s * Hkv + g) * acap + pos) * RV + c;
+    ak[dst] = k_rows[src];
+    av[dst] = v_rows[src];
+  }
+  __syncthreads();
+  if (answer_len && threadIdx.x == 0) answer_len[s] = pos + 1;
+}
+
+extern "C" int omni_append_answer(const void* k_rows, const void* v_rows, void* answer_k, void* answer_v, int batch,
+                                  int n_kv_heads, int head_dim, int acap, int n_answer, int32_t* answer_len,
+                                  void* stream) {
+  OMNI_CHECK(head_dim == dec::D, OMNI_E_SHAPE, "answer rows must have head_dim 128");
+  OMNI_CHECK(answer_len != nullptr || (n_answer >= 0 && n_answer < acap), OMNI_E_SHAPE, "answer capacity exhausted");
+  if (batch == 0) return OMNI_OK;
+  append_answer_kernel<<<batch, 128, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const uint4*>(k_rows), static_cast<const uint4*>(v_rows), static_cast<uint4*>(answer_k),
+      static_cast<uint4*>(answer_v), n_kv_heads, acap, n_answer, answer_len);
+  return omni_launch_check();
+}

@@ -223,17 +223,12 @@ def append_answer(cache: SlimKVCache, k_rows: torch.Tensor, v_rows: torch.Tensor
         if not grow:
             raise ShapeError("answer capacity exhausted")
         _grow_answer(cache, cache.n_answer + 1)
-    if cache.ragged:
-        b = torch.arange(cache.batch, device=k_rows.device)
-        pos = cache.answer_len_dev.long()
-        cache.answer_k[b, :, pos] = k_rows.to(torch.bfloat16)
-        cache.answer_v[b, :, pos] = v_rows.to(torch.bfloat16)
-        cache.answer_len_dev += 1
+    if cache.ragged:  # per-sequence rows answer_len[s], advanced on the device
+        ops.append_answer(k_rows, v_rows, cache.answer_k, cache.answer_v, 0, cache.answer_len_dev)
         cache.answer_lens = [a + 1 for a in cache.answer_lens]
         cache.n_answer = max(cache.answer_lens)
         return
-    cache.answer_k[:, :, cache.n_answer] = k_rows.to(torch.bfloat16)
-    cache.answer_v[:, :, cache.n_answer] = v_rows.to(torch.bfloat16)
+    ops.append_answer(k_rows, v_rows, cache.answer_k, cache.answer_v, cache.n_answer)
     cache.n_answer += 1
 
 

@@ -294,5 +294,14 @@ def decode_step_varlen(q, vision_k, vision_v, vision_len, text_k, text_v, text_l
     return out, flags
 
 
+def append_answer(k_rows, v_rows, answer_k, answer_v, n_answer: int, answer_len=None) -> None:
+    """One launch for the batch's new answer K / V rows (omni_append_answer)."""
+    b, hkv, d = k_rows.shape
+    kb = k_rows if k_rows.dtype == torch.bfloat16 else k_rows.to(torch.bfloat16)
+    vb = v_rows if v_rows.dtype == torch.bfloat16 else v_rows.to(torch.bfloat16)
+    _lib.call("omni_append_answer", _p(kb.contiguous()), _p(vb.contiguous()), _p(answer_k), _p(answer_v), b, hkv, d,
+              answer_k.shape[2], int(n_answer), _p(answer_len), _stream())
+
+
 def device_check() -> None:
     _lib.call("omni_device_check")
