@@ -130,8 +130,9 @@ __global__ void __launch_bounds__(128) decode_partial_kernel(
     const int32_t* __restrict__ vlen, const __nv_bfloat16* __restrict__ tk, const __nv_bfloat16* __restrict__ tv,
     const __nv_bfloat16* __restrict__ ak, const __nv_bfloat16* __restrict__ av, SegLens sl, int Hq, int Hkv,
     int vcap, int acap, const uint8_t* __restrict__ flags, float* __restrict__ part_ml, float* __restrict__ part_acc,
-    int n_chunks) {
+    int n_chunks, int* __restrict__ degenerate) {
   __shared__ float s_ml[4][MAXREP][2];
+  if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && threadIdx.x == 0) *degenerate = 0;  // for the merge
   __shared__ float s_acc[4][MAXREP][D];
   const int c = blockIdx.x, g = blockIdx.y, s = blockIdx.z;
   const int rep = Hq / Hkv;
@@ -445,7 +446,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1) decode_partial_tma_kernel(
     const __grid_constant__ CUtensorMap tm_ak, const __grid_constant__ CUtensorMap tm_av,
     const __nv_bfloat16* __restrict__ q, const int32_t* __restrict__ vlen, SegLens sl, int Hq, int Hkv,
     int vcap, int acap, const uint8_t* __restrict__ flags, float* __restrict__ part_ml,
-    float* __restrict__ part_acc, int n_chunks, int total_items, FuseArgs fa) {
+    float* __restrict__ part_acc, int n_chunks, int total_items, FuseArgs fa, int* __restrict__ degenerate) {
   extern __shared__ uint8_t dsm_raw[];
   __shared__ __align__(8) uint64_t full_bar[NSTG], empty_bar[NSTG];
   __shared__ __align__(8) uint64_t item_full[NIT], item_empty[NIT];
@@ -456,6 +457,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1) decode_partial_tma_kernel(
   uint8_t* dsm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dsm_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t sbase = smem_u32(dsm);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *degenerate = 0;  // reset for the merge kernel that follows
   if (threadIdx.x == 0) {
     for (int i = 0; i < NSTG; ++i) {
       mbar_init(smem_u32(&full_bar[i]), 1);
@@ -713,7 +715,6 @@ static int decode_step_impl(const void* q, const void* vision_k, const void* vis
     return (e && strcmp(e, "regs") == 0) ? 2 : (e && strcmp(e, "split") == 0) ? 1 : 0;
   }();
   const bool regs = impl == 2, fused = impl == 0;
-  OMNI_CUDA_TRY(cudaMemsetAsync(degenerate, 0, sizeof(int), st));
   if (!fused)
     dec::decode_flags_kernel<<<dim3(n_kv_heads, batch), 32, 0, st>>>(static_cast<const __nv_bfloat16*>(q), k_lazy,
                                                                       k_act, n_q_heads, n_kv_heads, tau,
@@ -724,7 +725,7 @@ static int decode_step_impl(const void* q, const void* vision_k, const void* vis
         static_cast<const __nv_bfloat16*>(vision_v), vision_len, static_cast<const __nv_bfloat16*>(text_k),
         static_cast<const __nv_bfloat16*>(text_v), static_cast<const __nv_bfloat16*>(answer_k),
         static_cast<const __nv_bfloat16*>(answer_v), sl, n_q_heads, n_kv_heads, vcap, acap, flags, part_ml,
-        part_acc, nc);
+        part_acc, nc, degenerate);
   } else {
     CUtensorMap m[6];
     const uint64_t vrows = (uint64_t)batch * n_kv_heads * vcap;
@@ -751,7 +752,7 @@ static int decode_step_impl(const void* q, const void* vision_k, const void* vis
     const dec::FuseArgs fa{k_lazy, k_act, tau, preserve_first_head, flags_override, flags};
     kern<<<min(sms, items), (dec::NCW + 1) * 32, dec::TSMEM, st>>>(
         m[0], m[1], m[2], m[3], m[4], m[5], static_cast<const __nv_bfloat16*>(q), vision_len, sl, n_q_heads,
-        n_kv_heads, vcap, acap, flags, part_ml, part_acc, nc, items, fa);
+        n_kv_heads, vcap, acap, flags, part_ml, part_acc, nc, items, fa, degenerate);
   }
   dec::decode_combine_kernel<<<dim3(n_q_heads, batch), dec::D, 0, st>>>(part_ml, part_acc, nc, out, degenerate);
   int st_code = omni_launch_check();
