@@ -49,3 +49,57 @@ def test_c3_128k_fused_probe_matches_materialised_and_outputs_finite():
     assert res.outputs.shape == Q.shape and bool(torch.isfinite(res.outputs).all())
     b = int(res.selection.info[0])
     assert 0.3 < b / n < 0.7
+
+
+def test_c5_decode_64k_matches_fp32_reference():
+    """C5 context length (64K, 28/4 heads), a batch of two sequences with their
+    own budgets: the slim-cache decode step equals an fp32 torch attention
+    over exactly the fetched keys (vision rows of the group iff the head is
+    active, then text and answer), heads classified exactly as the float64
+    two-logit rule says."""
+    from paper_2511_12201_b200 import decode as gdec
+    from paper_2511_12201_b200.synthetic import decode_queries_device, unit_vision_mean
+
+    n, nt = 65536, 64
+    nv = n - nt
+    hq, hkv, d = 28, 4, 128
+    cfg = SparsityConfig()
+    caches, means = [], []
+    for s in range(2):
+        Q, K, V = generate_device(hq, hkv, d, nv, nt, seed=40 + s)
+        k_lazy, k_act, _, _, _, _, _, _, mass, sel = select_device(Q, K, nv, cfg)
+        b = min(int(sel.info[0]), nv)
+        vsel = ops.select(mass, hkv, n, 256, cfg.p, "token", vision_limit=nv, budget_override=b)
+        caches.append(gdec.build_cache(K, V, vsel.selected, b, nv, nt, k_lazy, k_act, hq, answer_capacity=8))
+        means.append(unit_vision_mean(K, nv))
+        del Q, K, V
+    cache = gdec.stack_caches(caches)
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(5)
+    for t in range(3):
+        q = decode_queries_device(hq, hkv, means, [0, 1], 0.5, t)
+        out, fl = gdec.decode_attention(q, cache, cfg.tau)
+        rep = hq // hkv
+        scale = 1.0 / np.sqrt(d)
+        for s in range(2):
+            b = cache.budgets[s]
+            for h in range(hq):
+                g = h // rep
+                # float64 classification (query_select.py:63-68) on the same bf16 query
+                qd = q[s, h].double()
+                l0 = float(qd @ cache.k_lazy[s, g]) * scale
+                l1 = float(qd @ cache.k_act[s, g]) * scale
+                p_act = 1.0 / (1.0 + np.exp(l0 - l1))
+                exp_flag = bool(p_act > cfg.tau) or h == 0
+                assert bool(fl[s, h]) == exp_flag, (t, s, h, p_act)
+                keys = [cache.text_k[s, g, :nt], cache.answer_k[s, g, :cache.n_answer]]
+                vals = [cache.text_v[s, g, :nt], cache.answer_v[s, g, :cache.n_answer]]
+                if exp_flag:
+                    keys.insert(0, cache.vision_k[s, g, :b])
+                    vals.insert(0, cache.vision_v[s, g, :b])
+                Kc, Vc = torch.cat(keys).float(), torch.cat(vals).float()
+                w = torch.softmax((Kc @ q[s, h].float()) * scale, dim=0)
+                ref = w @ Vc
+                torch.testing.assert_close(out[s, h], ref, atol=5e-3, rtol=2e-2)
+        gdec.append_answer(cache, torch.randn(2, hkv, d, generator=gen, device="cuda"),
+                           torch.randn(2, hkv, d, generator=gen, device="cuda"))
