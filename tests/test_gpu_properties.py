@@ -103,3 +103,47 @@ def test_c5_decode_64k_matches_fp32_reference():
                 torch.testing.assert_close(out[s, h], ref, atol=5e-3, rtol=2e-2)
         gdec.append_answer(cache, torch.randn(2, hkv, d, generator=gen, device="cuda"),
                            torch.randn(2, hkv, d, generator=gen, device="cuda"))
+
+
+def test_c4_backward_32k_one_head_matches_fp32_autograd():
+    """C4 shapes (32K tokens, 28/4 heads): with the upstream gradient nonzero on
+    one head only, dQ of that head and dK / dV of its group equal an fp32
+    torch-autograd restatement of sparse_head_attention (prefill.py:89-122) on
+    the same bf16 inputs and selection (relative Frobenius error < 2e-2)."""
+    from paper_2511_12201_b200.autograd import SparseAttentionFn, plan_from_selection
+
+    n, nt = 32768, 64
+    nv = n - nt
+    hq, hkv, d, h = 28, 4, 128, 9
+    g = h // (hq // hkv)
+    Q, K, V = generate_device(hq, hkv, d, nv, nt, seed=17)
+    with torch.no_grad():
+        _, _, _, active, _, _, rows, counts, _, sel = select_device(Q, K, nv, SparsityConfig())
+    plan = plan_from_selection(rows, counts, sel, 0)
+    Qg, Kg, Vg = (x.clone().requires_grad_(True) for x in (Q, K, V))
+    dO = torch.zeros_like(Q)
+    dO[h] = torch.randn(n, d, device="cuda", dtype=torch.bfloat16)
+    SparseAttentionFn.apply(Qg, Kg, Vg, plan).backward(dO)
+
+    b = int(sel.counts[g])
+    idx = sel.selected[g, :b].long()
+    act = torch.nonzero(active[h].bool()).squeeze(1)
+    qa = Q[h, act].float().requires_grad_(True)
+    ks = K[g, idx].float().requires_grad_(True)
+    vs = V[g, idx].float().requires_grad_(True)
+    vis = idx[None, :] <= act[:, None]
+    s = (qa @ ks.T) / np.sqrt(d)
+    s = s.masked_fill(~vis, float("-inf"))
+    has = vis.any(dim=1)
+    p = torch.softmax(torch.where(has[:, None], s, torch.zeros_like(s)), dim=1) * has[:, None]
+    o = p @ vs
+    (o * dO[h, act].float()).sum().backward()
+    rel = lambda a, r: float((a.float() - r).norm() / r.norm())
+    assert rel(Qg.grad[h, act], qa.grad) < 2e-2
+    assert rel(Kg.grad[g, idx], ks.grad) < 2e-2
+    dv_ref = torch.zeros(n, d, device="cuda")
+    dv_ref[idx] = vs.grad
+    dv_ref[0] += dO[h, act][~has].float().sum(dim=0)  # rows with no visible key copy V[sink]
+    assert rel(Vg.grad[g], dv_ref) < 2e-2
+    others = [x for x in range(hq) if x != h]
+    assert not Qg.grad[others].float().abs().sum().item()
