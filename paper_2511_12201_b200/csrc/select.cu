@@ -122,15 +122,16 @@ __global__ void __launch_bounds__(256) probe_mass_fused_kernel(const double* __r
   constexpr int d = 128, ld = d + 2;  // +2 doubles: 16-byte aligned rows, staggered banks
   extern __shared__ double psm[];
   double* sq = psm;                   // [16][ld]
-  double* sk = sq + PF_ROWS * ld;     // [64][ld]
-  double* S = sk + PF_JT * ld;        // [16][nb]
+  double* skb = sq + PF_ROWS * ld;    // [2][64][ld]: key tiles, double-buffered
+  double* S = skb + 2 * PF_JT * ld;   // [16][nb]
   __shared__ double s_m[PF_ROWS], s_l[PF_ROWS];
   const int h = blockIdx.y, g = h / rep;
   const int I0 = blockIdx.x * PF_ROWS;
   const int jmax = min(nb, I0 + PF_ROWS);  // key blocks visible to the CTA's last row
   const double scale = 1.0 / sqrt(static_cast<double>(d));
   // global -> shared copies as 16-byte cp.async (all of a thread's chunks in
-  // flight at once; padded rows keep the micro-tile reads conflict-free)
+  // flight at once; padded rows keep the micro-tile reads conflict-free), one
+  // commit group per call
   auto copy_rows = [&](double* dst, const double* src, int rows, int valid) {
     for (int e = threadIdx.x; e < rows * (d / 2); e += blockDim.x) {
       const int i = e / (d / 2), c2 = e % (d / 2);
@@ -143,14 +144,21 @@ __global__ void __launch_bounds__(256) probe_mass_fused_kernel(const double* __r
         dp[1] = 0.0;
       }
     }
-    asm volatile("cp.async.wait_all;" ::: "memory");
+    asm volatile("cp.async.commit_group;" ::: "memory");
   };
   copy_rows(sq, pq + ((size_t)h * nb + I0) * d, PF_ROWS, min(PF_ROWS, nb - I0));
+  copy_rows(skb, pk + (size_t)g * nb * d, PF_JT, min(PF_JT, nb));
   // thread -> rows {ti, ti + 8}, key blocks {tj, tj + 32} of the 64-wide tile
   const int ti = threadIdx.x >> 5, tj = threadIdx.x & 31;
-  for (int jt = 0; jt < jmax; jt += PF_JT) {
-    __syncthreads();
-    copy_rows(sk, pk + ((size_t)g * nb + jt) * d, PF_JT, min(PF_JT, nb - jt));
+  for (int jt = 0, it = 0; jt < jmax; jt += PF_JT, ++it) {
+    double* sk = skb + (it & 1) * PF_JT * ld;
+    if (jt + PF_JT < jmax) {  // the next key tile streams in while this one is used
+      copy_rows(skb + ((it + 1) & 1) * PF_JT * ld, pk + ((size_t)g * nb + jt + PF_JT) * d, PF_JT,
+                min(PF_JT, nb - jt - PF_JT));
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
     __syncthreads();
     double a00 = 0.0, a01 = 0.0, a10 = 0.0, a11 = 0.0;
     const double* q0 = sq + ti * ld;
@@ -169,6 +177,7 @@ __global__ void __launch_bounds__(256) probe_mass_fused_kernel(const double* __r
     const int J0 = jt + tj, J1 = jt + tj + 32;
     if (J0 < nb) { S[ti * nb + J0] = a00 * scale; S[(ti + 8) * nb + J0] = a10 * scale; }
     if (J1 < nb) { S[ti * nb + J1] = a01 * scale; S[(ti + 8) * nb + J1] = a11 * scale; }
+    __syncthreads();  // every thread is done with this buffer before it is refilled
   }
   __syncthreads();
   // masked softmax statistics of each row over J <= I (warp per two rows)
@@ -673,7 +682,7 @@ extern "C" int omni_probe_mass(const double* pooled_q, const double* pooled_k, i
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int ntiles = (n_blocks + PF_ROWS - 1) / PF_ROWS;
   double* partial = static_cast<double*>(workspace);  // [Hq, ntiles, nb] <= [Hq, nb, nb + 2]
-  const int shm = (int)sizeof(double) * ((PF_ROWS + PF_JT) * (128 + 2) + PF_ROWS * n_blocks);
+  const int shm = (int)sizeof(double) * ((PF_ROWS + 2 * PF_JT) * (128 + 2) + PF_ROWS * n_blocks);
   static int attr = 0;
   if (shm > attr) {
     OMNI_CUDA_TRY(cudaFuncSetAttribute(probe_mass_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, shm));
