@@ -33,8 +33,26 @@ class SelectionResult:
 
 
 @dataclass
+class KeyScores:
+    """kv_select.py:23-36 under rule B: one token-level score vector per KV
+    group (block-constant on the probe path) and its kurtosis."""
+
+    scores: list
+    kurtoses: list
+
+    @property
+    def num_heads(self) -> int:
+        return len(self.scores)
+
+    @property
+    def num_keys(self) -> int:
+        return self.scores[0].shape[0]
+
+
+@dataclass
 class PrefillOutput:
-    """reference prefill.py:68-86 (without op counters / recall)."""
+    """reference prefill.py:68-86 without the op counters; ``recall_per_head``
+    (metrics.py:26-39, GPU LSE identity) is filled when requested."""
 
     outputs: list
     query_masks: list
@@ -44,6 +62,8 @@ class PrefillOutput:
     flattest_total_mass: float
     score_source: str
     device: DevicePrefill | None = field(default=None, repr=False)
+    key_scores: KeyScores | None = None
+    recall_per_head: list | None = None
 
     @property
     def active_per_head(self) -> list:
@@ -51,7 +71,7 @@ class PrefillOutput:
 
 
 def sparse_prefill(w: AttentionWorkload, cfg: SparsityConfig = SparsityConfig(),
-                   score_source: str = "exact") -> PrefillOutput:
+                   score_source: str = "exact", with_recall: bool = False) -> PrefillOutput:
     """Query masks -> probe key scores -> flattest-group budget -> per-group
     top-b -> sparse attention (reference prefill.py:142-192 under rule B).
     The block-probe score source is the hot path; "exact" computes the
@@ -70,8 +90,17 @@ def sparse_prefill(w: AttentionWorkload, cfg: SparsityConfig = SparsityConfig(),
     selected = [sel[g, :b].astype(np.int64) for g in range(hkv)]
     outs = list(res.outputs.float().cpu().numpy().astype(np.float64))
     masks = list(res.active.cpu().numpy().astype(bool))
+    n = Q.shape[1]
+    gs = res.selection.group_scores.cpu().numpy()
+    blk = 1 if gs.shape[1] == n else cfg.block_size
+    scores = [np.repeat(gs[g], blk)[:n] for g in range(hkv)]  # block-constant per-token scores
+    recall = None
+    if with_recall:
+        from .metrics import attention_recall_device
+
+        recall = attention_recall_device(res, Q, K, V, w.layout.sink_index).cpu().tolist()
     return PrefillOutput(outs, masks, SelectionResult(b, selected, flat), list(stats[:hkv]), float(stats[hkv]),
-                         float(stats[hkv + 1]), score_source, res)
+                         float(stats[hkv + 1]), score_source, res, KeyScores(scores, list(stats[:hkv])), recall)
 
 
 def sparse_head_attention(q, k, v, selected, active, sink_index: int):

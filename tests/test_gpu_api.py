@@ -109,3 +109,26 @@ def test_sparse_prefill_and_head_attention_api():
                                                                   ref.active[1], 0), atol=2e-2, rtol=2e-2)
     empty = sparse_head_attention(Qb[1], Kb[0], Vb[0], np.array([], dtype=np.int64), ref.active[1], 0)
     assert not empty.any()  # prefill.py:107-108
+
+
+def test_prefill_output_key_scores_and_recall():
+    """PrefillOutput.key_scores (kv_select.py:23-36, rule B: per KV group) and
+    recall_per_head (metrics.py:26-39) vs the oracle on the same inputs."""
+    from oracle import metrics as om
+    from oracle import pipeline as opipe
+    from oracle.workload import round_bf16
+    from paper_2511_12201_b200.attention import AttentionWorkload, TokenLayout
+    from paper_2511_12201_b200.prefill import SparsityConfig, sparse_prefill
+
+    Q, K, V = generate(Spec(heads=4, heads_kv=2, head_dim=128, n_vision=1500, n_text=36, seed=8))
+    Qb, Kb, Vb = round_bf16(Q), round_bf16(K), round_bf16(V)
+    w = AttentionWorkload(list(Qb), list(Kb), list(Vb), TokenLayout(1500, 36))
+    out = sparse_prefill(w, SparsityConfig(), "probe", with_recall=True)
+    ref = opipe.select(Qb, Kb, 1500, 0, 0.08, 0.82, 256)
+    assert out.key_scores.num_heads == 2 and out.key_scores.num_keys == 1536
+    for g in range(2):
+        np.testing.assert_allclose(out.key_scores.scores[g], ref.group_scores[g], rtol=1e-10, atol=1e-14)
+    np.testing.assert_allclose(out.key_scores.kurtoses, ref.kurtoses, rtol=1e-10)
+    for h in range(4):
+        exp = om.head_recall(Qb[h], Kb[h // 2], ref.selected[h // 2], ref.active[h])
+        assert abs(out.recall_per_head[h] - exp) < 2e-3
