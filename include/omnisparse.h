@@ -242,6 +242,13 @@ int omni_decode_step_varlen(const void* q, const void* vision_k, const void* vis
 int omni_append_answer(const void* k_rows, const void* v_rows, void* answer_k, void* answer_v, int batch,
                        int n_kv_heads, int head_dim, int acap, int n_answer, int32_t* answer_len, void* stream);
 
+/* classify_decode_query (decode.py:124-140) for a batch: q bf16 [B, Hq, d],
+ * k_lazy / k_act f64 [B, Hkv, d] -> flags u8 [B, Hq] (float64 two-logit
+ * rule, head 0 forced active under preserve_first_head).                   */
+int omni_decode_flags(const void* q, const double* k_lazy, const double* k_act, int batch, int n_q_heads,
+                      int n_kv_heads, int head_dim, double tau, int preserve_first_head, uint8_t* flags,
+                      void* stream);
+
 /* omni_decode (SURVEY §8b's name for K7): identical to omni_decode_step.   */
 int omni_decode(const void* q, const void* vision_k, const void* vision_v, const int32_t* vision_len,
                 const void* text_k, const void* text_v, int n_text, const void* answer_k, const void* answer_v,

@@ -53,6 +53,7 @@ SIGNATURES = {
     "omni_decode": (_c_int, [_p, _p, _p, _p, _p, _p, _c_int, _p, _p, _c_int, _p, _p, _c_int, _c_int,
                              _c_int, _c_int, _c_int, _c_int, _c_double, _c_int, _p, _p, _p, _p, _p]),
     "omni_append_answer": (_c_int, [_p, _p, _p, _p, _c_int, _c_int, _c_int, _c_int, _c_int, _p, _p]),
+    "omni_decode_flags": (_c_int, [_p, _p, _p, _c_int, _c_int, _c_int, _c_int, _c_double, _c_int, _p, _p]),
     "omni_slim_cache": (_c_int, [_p, _p, _c_int, _c_int, _c_int, _c_int, _p, _c_int, _c_int, _c_int, _p, _p, _p]),
     "omni_decode_step_varlen": (_c_int, [_p, _p, _p, _p, _p, _p, _p, _c_int, _p, _p, _p, _p, _p, _c_int, _c_int,
                                          _c_int, _c_int, _c_int, _c_int, _c_double, _c_int, _p, _p, _p, _p, _p,

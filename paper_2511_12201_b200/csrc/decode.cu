@@ -840,3 +840,19 @@ extern "C" int omni_append_answer(const void* k_rows, const void* v_rows, void* 
       static_cast<uint4*>(answer_v), n_kv_heads, acap, n_answer, answer_len);
   return omni_launch_check();
 }
+
+// classify_decode_query (decode.py:124-140) alone: flags u8 [B, Hq] for one
+// decode token per sequence (the classification K7 also fuses).
+extern "C" int omni_decode_flags(const void* q, const double* k_lazy, const double* k_act, int batch, int n_q_heads,
+                                 int n_kv_heads, int head_dim, double tau, int preserve_first_head, uint8_t* flags,
+                                 void* stream) {
+  OMNI_CHECK(head_dim == dec::D, OMNI_E_SHAPE, "decode classification requires head_dim == 128");
+  OMNI_CHECK(n_kv_heads >= 1 && n_q_heads % n_kv_heads == 0 && n_q_heads / n_kv_heads <= dec::MAXREP, OMNI_E_SHAPE,
+             "need Hq a multiple of Hkv with at most 8 Q heads per group");
+  OMNI_CHECK(tau >= 0.0 && tau < 1.0, OMNI_E_PARAM, "tau must be in [0, 1)");
+  if (batch == 0) return OMNI_OK;
+  dec::decode_flags_kernel<<<dim3(n_kv_heads, batch), 32, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const __nv_bfloat16*>(q), k_lazy, k_act, n_q_heads, n_kv_heads, tau, preserve_first_head, nullptr,
+      flags);
+  return omni_launch_check();
+}

@@ -232,6 +232,17 @@ def append_answer(cache: SlimKVCache, k_rows: torch.Tensor, v_rows: torch.Tensor
     cache.n_answer += 1
 
 
+def classify_decode_query(q: torch.Tensor, cache: SlimKVCache, tau: float) -> torch.Tensor:
+    """decode.py:124-140 for a batch: u8 [B, Hq] active flags of one decode
+    token per sequence (the classification decode_attention also runs)."""
+    if q.shape != (cache.batch, cache.n_q_heads, cache.head_dim):
+        raise ShapeError(f"decode query must be [B, Hq, d], got {tuple(q.shape)}")
+    qb = (q if q.dtype == torch.bfloat16 else q.to(torch.bfloat16)).contiguous()
+    flags = torch.empty(cache.batch, cache.n_q_heads, device=q.device, dtype=torch.uint8)
+    ops.call_decode_flags(qb, cache.k_lazy, cache.k_act, cache.n_kv_heads, float(tau), cache.preserve_first_head, flags)
+    return flags
+
+
 def decode_attention(q: torch.Tensor, cache: SlimKVCache, tau: float, flags: torch.Tensor | None = None,
                      log: bool = True):
     """decode.py:157-194 for a batch: returns (out f32 [B, Hq, d], flags u8

@@ -140,3 +140,32 @@ def select_vision_keys(scores: KeyScores, budget: int, n_vision: int) -> Selecti
     sel, info, _ = _run(scores.scores, budget_override=b, vision_limit=n_vision)
     s = sel.selected.cpu().numpy()
     return SelectionResult(b, [s[g, :b].astype(np.int64) for g in range(scores.num_heads)], flattest_head(scores))
+
+
+def select_top_blocks(scores: KeyScores, budget: int, block_size: int) -> SelectionResult:
+    """kv_select.py:147-176: whole blocks ranked by summed token mass (ties to
+    the lower block), the marginal block contributing its lowest indices —
+    exactly ``budget`` keys per head. The block sums are the reference's
+    np.add.reduceat; ranking and the block table run on the GPU (K3b)."""
+    n = scores.num_keys
+    if not 1 <= budget <= n:
+        raise ParameterError(f"budget must be in [1, {n}], got {budget}")
+    if block_size < 1:
+        raise ParameterError(f"block size must be >= 1, got {block_size}")
+    starts = np.arange(0, n, block_size)
+    bm = np.stack([np.add.reduceat(np.asarray(a.cpu() if isinstance(a, torch.Tensor) else a, dtype=np.float64),
+                                   starts) for a in scores.scores])
+    h = bm.shape[0]
+    sel = ops.select(torch.from_numpy(bm).to("cuda"), h, n, block_size, 0.5, "block", budget_override=budget)
+    s = sel.selected.cpu().numpy()
+    return SelectionResult(budget, [s[g, :budget].astype(np.int64) for g in range(h)], flattest_head(scores))
+
+
+def sparsity_gap(scores: KeyScores, p: float) -> float:
+    """kv_select.py:198-210: (b_flattest - b_sharpest) / N with each head's
+    individual budget at retention ``p``."""
+    if scores.num_heads < 2:
+        raise ParameterError("sparsity gap needs at least two heads")
+    flat = flattest_head(scores)
+    sharp = int(np.argmax(scores.kurtoses))
+    return (determine_budget(scores.scores[flat], p) - determine_budget(scores.scores[sharp], p)) / scores.num_keys

@@ -303,5 +303,11 @@ def append_answer(k_rows, v_rows, answer_k, answer_v, n_answer: int, answer_len=
               answer_k.shape[2], int(n_answer), _p(answer_len), _stream())
 
 
+def call_decode_flags(q, k_lazy, k_act, n_kv_heads: int, tau: float, preserve_first_head: bool, flags) -> None:
+    b, hq, d = q.shape
+    _lib.call("omni_decode_flags", _p(q), _p(k_lazy), _p(k_act), b, hq, n_kv_heads, d, float(tau),
+              int(bool(preserve_first_head)), _p(flags), _stream())
+
+
 def device_check() -> None:
     _lib.call("omni_device_check")

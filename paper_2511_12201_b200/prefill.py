@@ -17,6 +17,7 @@ import torch
 from . import ops
 from .attention import AttentionWorkload
 from .errors import ParameterError, ShapeError
+from .kv_select import KeyScores
 from .pipeline import DevicePrefill, SparsityConfig, sparse_prefill_device  # noqa: F401  (re-export)
 
 SCORE_SOURCES = ("exact", "probe")
@@ -30,23 +31,6 @@ class SelectionResult:
     budget: int
     selected: list
     flattest_head: int
-
-
-@dataclass
-class KeyScores:
-    """kv_select.py:23-36 under rule B: one token-level score vector per KV
-    group (block-constant on the probe path) and its kurtosis."""
-
-    scores: list
-    kurtoses: list
-
-    @property
-    def num_heads(self) -> int:
-        return len(self.scores)
-
-    @property
-    def num_keys(self) -> int:
-        return self.scores[0].shape[0]
 
 
 @dataclass

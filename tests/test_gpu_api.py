@@ -132,3 +132,43 @@ def test_prefill_output_key_scores_and_recall():
     for h in range(4):
         exp = om.head_recall(Qb[h], Kb[h // 2], ref.selected[h // 2], ref.active[h])
         assert abs(out.recall_per_head[h] - exp) < 2e-3
+
+
+def test_select_top_blocks_sparsity_gap_and_decode_classification():
+    """kv_select.select_top_blocks / sparsity_gap (kv_select.py:147-210) and
+    decode.classify_decode_query (decode.py:124-140) vs the oracle."""
+    import torch
+
+    from paper_2511_12201_b200 import decode as gdec
+    from paper_2511_12201_b200 import kv_select as ks
+
+    rng = np.random.default_rng(3)
+    vecs = [rng.gamma(0.5 + i, size=1000) for i in range(3)]
+    scores = ks.key_scores_from_vectors(vecs)
+    for b, blk in ((1, 64), (300, 64), (257, 100), (1000, 128)):
+        got = ks.select_top_blocks(scores, b, blk)
+        exp = osel.top_blocks(vecs, b, blk)
+        for g in range(3):
+            np.testing.assert_array_equal(got.selected[g], exp[g])
+    for p in (0.2, 0.82):
+        assert ks.sparsity_gap(scores, p) == osel.sparsity_gap(vecs, p)
+    # decode classification: flags of decode_attention and the standalone call agree with the oracle rule
+    hq, hkv, d = 8, 2, 128
+    q = torch.randn(3, hq, d, device="cuda").to(torch.bfloat16)
+    k_lazy = torch.randn(3, hkv, d, device="cuda", dtype=torch.float64)
+    k_act = torch.randn(3, hkv, d, device="cuda", dtype=torch.float64)
+    cache = gdec.SlimKVCache(*(torch.zeros(3, hkv, 128, d, device="cuda", dtype=torch.bfloat16) for _ in range(2)),
+                             torch.full((3,), 64, device="cuda", dtype=torch.int32),
+                             torch.zeros(3, hkv, 128, device="cuda", dtype=torch.int32),
+                             *(torch.randn(3, hkv, 16, d, device="cuda").to(torch.bfloat16) for _ in range(2)),
+                             *(torch.zeros(3, hkv, 4, d, device="cuda", dtype=torch.bfloat16) for _ in range(2)),
+                             k_lazy, k_act, hq, True, budgets=[64] * 3)
+    fl = gdec.classify_decode_query(q, cache, 0.3).cpu().numpy().astype(bool)
+    _, fl2 = gdec.decode_attention(q, cache, 0.3, log=False)
+    np.testing.assert_array_equal(fl, fl2.cpu().numpy().astype(bool))
+    for s in range(3):
+        for h in range(hq):
+            g = h // (hq // hkv)
+            _, verdict = osel.classify(q[s, h].double().cpu().numpy()[None], k_lazy[s, g].cpu().numpy(),
+                                       k_act[s, g].cpu().numpy(), 0.3)
+            assert fl[s, h] == (bool(verdict[0]) or h == 0)
