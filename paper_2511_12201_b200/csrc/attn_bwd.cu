@@ -28,12 +28,12 @@ namespace bwd {
 
 constexpr int D = 128;
 // Exponential pairs (of 16 per 32-column chunk) evaluated by the FMA-pipe
-// polynomial instead of MUFU.EX2 in the dS math of dkv / dq (the MUFU is the
-// co-bottleneck there as in K4; measured at C4: 4 of 16 is best for both,
-// dkv 5.16 -> 4.68 ms); masked entries are discarded by a select, so the
-// polynomial's behaviour on them does not matter.
+// polynomial instead of MUFU.EX2 in the dS math (masked entries are discarded
+// by a select, so the polynomial's behaviour on them does not matter).
+// Measured at C4: dq 4 of 16 (MUFU co-bottleneck); dkv 0 since P^T is formed
+// off the critical path (4 of 16 was best before that change).
 #ifndef OMNI_BWD_POLY
-#define OMNI_BWD_POLY 4
+#define OMNI_BWD_POLY 0
 #endif
 #ifndef OMNI_DQ_POLY
 #define OMNI_DQ_POLY 4
