@@ -58,56 +58,63 @@ __global__ void __launch_bounds__(256) bwd_prep_kernel(
     const int32_t* __restrict__ sel, const int32_t* __restrict__ sel_counts, int N, int rep, int capq,
     __nv_bfloat16* __restrict__ Qc, __nv_bfloat16* __restrict__ dOc, float* __restrict__ lse2c,
     float* __restrict__ Dc, int32_t* __restrict__ visc, float* __restrict__ dv_sink) {
+  // one warp per 32 consecutive compacted rows: their visible-key counts by a
+  // warp-cooperative search (ascending rows), then the rows one by one
   const int h = blockIdx.y;
-  const int i = blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
+  const int i0 = (blockIdx.x * 8 + (threadIdx.x >> 5)) * 32;
   const int cnt = __ldg(counts + h);
   const int lim = ((cnt + 127) / 128) * 128;
-  if (i >= lim) return;
-  const size_t ci = (size_t)h * capq + i;
-  uint2* qd = reinterpret_cast<uint2*>(Qc + ci * D);
-  uint2* dd = reinterpret_cast<uint2*>(dOc + ci * D);
-  if (i >= cnt) {
-    qd[lane] = make_uint2(0, 0);
-    dd[lane] = make_uint2(0, 0);
-    if (lane == 0) {
-      lse2c[ci] = 0.f;
-      Dc[ci] = 0.f;
-      visc[ci] = 0;
-    }
-    return;
-  }
+  if (i0 >= lim) return;
   const int g = h / rep;
-  const int pos = __ldg(rows + (size_t)h * N + i);
-  const size_t src = ((size_t)h * N + pos) * D;
-  const uint2 qv = __ldg(reinterpret_cast<const uint2*>(Q + src) + lane);
-  const uint2 ov = __ldg(reinterpret_cast<const uint2*>(O + src) + lane);
-  const uint2 gv = __ldg(reinterpret_cast<const uint2*>(dO + src) + lane);
-  qd[lane] = qv;
-  dd[lane] = gv;
-  const __nv_bfloat162* o2 = reinterpret_cast<const __nv_bfloat162*>(&ov);
-  const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&gv);
-  float dsum = 0.f;
-  float gf[4];
-#pragma unroll
-  for (int k = 0; k < 2; ++k) {
-    const float2 a = __bfloat1622float2(o2[k]), b = __bfloat1622float2(g2[k]);
-    dsum += a.x * b.x + a.y * b.y;
-    gf[2 * k] = b.x;
-    gf[2 * k + 1] = b.y;
+  const int il = i0 + lane;
+  const bool lvalid = il < cnt;
+  const int lpos = lvalid ? __ldg(rows + (size_t)h * N + il) : 0;
+  int lvis = count_le_warp(sel + (size_t)g * N, __ldg(sel_counts + g), lpos, lvalid);
+  if (!lvalid) lvis = 0;
+  if (il < lim) {
+    const size_t ci = (size_t)h * capq + il;
+    lse2c[ci] = lvalid ? __ldg(lse + (size_t)h * N + lpos) * static_cast<float>(kLog2e) : 0.f;
+    visc[ci] = lvis;
   }
-  dsum = warp_sum(dsum);
-  int vis = 0;
-  if (lane == 0) {
-    vis = count_le(sel + (size_t)g * N, __ldg(sel_counts + g), pos);
-    Dc[ci] = dsum;
-    lse2c[ci] = __ldg(lse + (size_t)h * N + pos) * static_cast<float>(kLog2e);
-    visc[ci] = vis;
-  }
-  vis = __shfl_sync(0xffffffffu, vis, 0);
-  if (vis == 0) {  // forward copied V[sink] for this row: dV[sink] += dO
+#pragma unroll 4
+  for (int r = 0; r < 32; ++r) {
+    const int i = i0 + r;
+    if (i >= lim) break;
+    const size_t ci = (size_t)h * capq + i;
+    uint2* qd = reinterpret_cast<uint2*>(Qc + ci * D);
+    uint2* dd = reinterpret_cast<uint2*>(dOc + ci * D);
+    if (i >= cnt) {
+      qd[lane] = make_uint2(0, 0);
+      dd[lane] = make_uint2(0, 0);
+      if (lane == 0) Dc[ci] = 0.f;
+      continue;
+    }
+    const int pos = __shfl_sync(0xffffffffu, lpos, r);
+    const int vis = __shfl_sync(0xffffffffu, lvis, r);
+    const size_t src = ((size_t)h * N + pos) * D;
+    const uint2 qv = __ldg(reinterpret_cast<const uint2*>(Q + src) + lane);
+    const uint2 ov = __ldg(reinterpret_cast<const uint2*>(O + src) + lane);
+    const uint2 gv = __ldg(reinterpret_cast<const uint2*>(dO + src) + lane);
+    qd[lane] = qv;
+    dd[lane] = gv;
+    const __nv_bfloat162* o2 = reinterpret_cast<const __nv_bfloat162*>(&ov);
+    const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&gv);
+    float dsum = 0.f;
+    float gf[4];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) atomicAdd(dv_sink + (size_t)g * D + lane * 4 + k, gf[k]);
+    for (int k = 0; k < 2; ++k) {
+      const float2 a2 = __bfloat1622float2(o2[k]), b2 = __bfloat1622float2(g2[k]);
+      dsum += a2.x * b2.x + a2.y * b2.y;
+      gf[2 * k] = b2.x;
+      gf[2 * k + 1] = b2.y;
+    }
+    dsum = warp_sum(dsum);
+    if (lane == 0) Dc[ci] = dsum;
+    if (vis == 0) {  // forward copied V[sink] for this row: dV[sink] += dO
+#pragma unroll
+      for (int k = 0; k < 4; ++k) atomicAdd(dv_sink + (size_t)g * D + lane * 4 + k, gf[k]);
+    }
   }
 }
 
@@ -1045,7 +1052,7 @@ extern "C" int omni_sparse_attn_bwd_ex(const void* Q, const void* K_sel, const v
   OMNI_CUDA_TRY(cudaMemsetAsync(dK_sel, 0, sizeof(float) * (size_t)n_kv_heads * cap * head_dim, st));
   OMNI_CUDA_TRY(cudaMemsetAsync(dV_sel, 0, sizeof(float) * (size_t)n_kv_heads * cap * head_dim, st));
   OMNI_CUDA_TRY(cudaMemsetAsync(dV_sink, 0, sizeof(float) * (size_t)n_kv_heads * head_dim, st));
-  bwd::bwd_prep_kernel<<<dim3(capq / 8, n_q_heads), 256, 0, st>>>(
+  bwd::bwd_prep_kernel<<<dim3((capq + 255) / 256, n_q_heads), 256, 0, st>>>(
       static_cast<const __nv_bfloat16*>(Q), static_cast<const __nv_bfloat16*>(O),
       static_cast<const __nv_bfloat16*>(dO), lse, rows, counts, selected, sel_counts, seq_len, rep, capq, Qc, dOc,
       lse2c, Dc, visc, dV_sink);

@@ -591,6 +591,50 @@ __device__ __forceinline__ int count_le(const int32_t* __restrict__ a, int n, in
   return lo;
 }
 
+// count_le for the 32 ascending keys of a warp (invalid lanes: any key,
+// result unused), warp-cooperatively: a 32-ary search for the first element
+// >= the smallest key (one round of 32 parallel loads per level instead of 5
+// dependent binary-search steps), then a scan of the window up to the
+// largest key, 32 elements per load.
+__device__ __forceinline__ int count_le_warp(const int32_t* __restrict__ a, int n, int key, bool valid) {
+  const int lane = threadIdx.x & 31;
+  int kmin = valid ? key : INT_MAX, kmax = valid ? key : INT_MIN;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, o));
+    kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
+  }
+  if (kmin == INT_MAX) return 0;
+  int lo = 0, hi = n;  // the first index with a[k] >= kmin lies in [lo, hi]
+  while (hi - lo > 32) {
+    const int step = (hi - lo + 31) >> 5;
+    const int idx = lo + lane * step;
+    const int v = idx < hi ? __ldg(a + idx) : INT_MAX;
+    const int k = __popc(__ballot_sync(0xffffffffu, v < kmin));  // pivots below kmin (a prefix)
+    const int nlo = k == 0 ? lo : lo + (k - 1) * step + 1;
+    hi = min(hi, lo + k * step);
+    lo = nlo;
+  }
+  {
+    const int idx = lo + lane;
+    const int v = idx < hi ? __ldg(a + idx) : INT_MAX;
+    lo += __popc(__ballot_sync(0xffffffffu, v < kmin));
+  }
+  int c = lo;  // every element below lo is < kmin <= key
+  for (int base = lo; base < n; base += 32) {
+    const int idx = base + lane;
+    const int v = idx < n ? __ldg(a + idx) : INT_MAX;
+#pragma unroll 8
+    for (int q = 0; q < 32; ++q) {
+      const int kq = __shfl_sync(0xffffffffu, key, q);
+      const int cnt = __popc(__ballot_sync(0xffffffffu, v <= kq));
+      if (lane == q) c += cnt;
+    }
+    if (__shfl_sync(0xffffffffu, v, 31) > kmax) break;  // the window is exhausted
+  }
+  return c;
+}
+
 template <typename T>
 __device__ __forceinline__ T warp_sum(T v) {
 #pragma unroll
