@@ -77,7 +77,7 @@ __global__ void __launch_bounds__(256) bwd_prep_kernel(
     lse2c[ci] = lvalid ? __ldg(lse + (size_t)h * N + lpos) * static_cast<float>(kLog2e) : 0.f;
     visc[ci] = lvis;
   }
-#pragma unroll 4
+#pragma unroll 8
   for (int r = 0; r < 32; ++r) {
     const int i = i0 + r;
     if (i >= lim) break;
