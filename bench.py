@@ -254,51 +254,59 @@ def cpu_reference_sample(Q, K, V, n_vision, tau, p, head=13, rows_sample=1024, s
 
 
 # ------------------------------------------------------------------ decode
-def decode_section(args, steps, warmup, hbm_peak, tau=None, p=None, dense=True):
+def decode_section(args, steps, warmup, hbm_peak, tau=None, p=None, dense=True, world=1, rank=0):
+    """C5: batch-32 decode over 64K-token slim caches. At N > 1 the batch is
+    sequence-sharded (parallel.sequence_shard: rank r decodes its own
+    sequences from its own caches, no collective); the step time is the max
+    over ranks and tok/s counts the whole batch."""
     import torch
 
     from paper_2511_12201_b200 import decode as gdec
-    from paper_2511_12201_b200 import ops
-    from paper_2511_12201_b200.pipeline import SparsityConfig, select_device
+    from paper_2511_12201_b200.parallel import sequence_shard
+    from paper_2511_12201_b200.pipeline import SparsityConfig
     from paper_2511_12201_b200.synthetic import decode_queries_device, generate_device, unit_vision_mean
 
     n = args.seq
     nv = n - N_TEXT
-    B = args.decode_batch
+    B_all = args.decode_batch
+    seqs = list(sequence_shard(B_all, world, rank))
+    B = len(seqs)
     tau = args.tau if tau is None else tau
     p = args.p if p is None else p
     cfg = SparsityConfig(tau=tau, p=p)
     caches, k_means = [], []
-    for s in range(B):
+    # one page-pool reservation for the whole batch (pages of 64 rows: ~0.47 N
+    # vision rows per group at the defaults, text and answer pages)
+    gdec.default_pool(torch.device("cuda")).reserve(B * HKV * (-(-int(0.6 * nv) // 64) + 4))
+    for s in seqs:
         Q, K, V = generate_device(HQ, HKV, D, nv, N_TEXT, seed=1000 + s, lazy_fraction=args.lazy)
-        k_lazy, k_act, pk, active, _, pq, rows, counts, mass, sel = select_device(Q, K, nv, cfg)
-        b = int(sel.info[0])
-        vsel = ops.select(mass, HKV, n, cfg.block_size, cfg.p, "token", vision_limit=nv, budget_override=b)
-        bv = min(b, nv)
-        caches.append(gdec.build_cache(K, V, vsel.selected, bv, nv, N_TEXT, k_lazy, k_act, HQ,
-                                       answer_capacity=warmup + steps + 8))
+        caches.append(gdec.cache_from_prompt(Q, K, V, nv, N_TEXT, cfg, answer_capacity=warmup + steps + 8))
         k_means.append(unit_vision_mean(K, nv))
-        del Q, K, V, pq, pk, rows, active
+        del Q, K, V
     torch.cuda.empty_cache()
     cache = gdec.stack_caches(caches)
     del caches
     torch.cuda.empty_cache()
     n_steps = warmup + steps
-    qs = [decode_queries_device(HQ, HKV, k_means, range(B), args.lazy, t) for t in range(n_steps)]
+    qs = [decode_queries_device(HQ, HKV, k_means, seqs, args.lazy, t) for t in range(n_steps)]
     gen = torch.Generator(device="cuda")
-    gen.manual_seed(7)
+    gen.manual_seed(7 + rank)
     kv_new = [(torch.randn(B, HKV, D, generator=gen, device="cuda").bfloat16(),
                torch.randn(B, HKV, D, generator=gen, device="cuda").bfloat16()) for _ in range(n_steps)]
     flags_log = []
 
     def step(t):
-        out, fl = gdec.decode_attention(qs[t], cache, tau, log=False)
+        out, fl = gdec.decode_attention_batch(qs[t], cache, tau, log=False)
         flags_log.append(fl)
-        gdec.append_answer(cache, *kv_new[t])
+        gdec.append_answer_batch(cache, *kv_new[t])
 
     for t in range(warmup):
         step(t)
     torch.cuda.synchronize()
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     flags_log.clear()
     e0.record()
@@ -317,22 +325,38 @@ def decode_section(args, steps, warmup, hbm_peak, tau=None, p=None, dense=True):
     slim_bytes = (tot_vis + tot_ta) / steps
     full_bytes = B * HKV * (n + n_ans0 + steps / 2) * 2 * D * 2
     q_bytes = B * HQ * D * (2 + 4)
+    fetched = float(torch.stack([f.view(B, HKV, -1).any(dim=2) for f in flags_log]).float().mean())
+    budgets = sum(cache.budgets)
+    if world > 1:  # max time over ranks, bytes summed over ranks
+        import torch.distributed as dist
+
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        v = torch.tensor([slim_bytes, full_bytes, q_bytes, fetched * B, budgets], device="cuda", dtype=torch.float64)
+        dist.all_reduce(v, op=dist.ReduceOp.SUM)
+        ms = float(t)
+        slim_bytes, full_bytes, q_bytes, fetched, budgets = (float(x) for x in v)
+        fetched /= B_all
     res = {
-        "batch": B, "context": n, "ms_per_step": ms, "tok_s": B / (ms / 1e3),
+        "batch": B_all, "context": n, "ms_per_step": ms, "tok_s": B_all / (ms / 1e3),
         "kv_bytes_per_step": slim_bytes, "full_cache_bytes_per_step": full_bytes,
         "kv_bytes_reduction": full_bytes / slim_bytes,
-        "budgets_mean": sum(cache.budgets) / B,
-        "fetched_group_frac": float(torch.stack([f.view(B, HKV, -1).any(dim=2) for f in flags_log]).float().mean()),
-        "roofline": {"bound": "hbm", "achieved": (slim_bytes + q_bytes) / (ms / 1e3) / 1e9, "peak": hbm_peak,
-                     "unit": "GB/s", "frac": (slim_bytes + q_bytes) / (ms / 1e3) / 1e9 / hbm_peak},
+        "budgets_mean": budgets / B_all,
+        "fetched_group_frac": fetched,
+        "roofline": {"bound": "hbm", "achieved": (slim_bytes + q_bytes) / (ms / 1e3) / 1e9 / world,
+                     "peak": hbm_peak, "unit": "GB/s per GPU",
+                     "frac": (slim_bytes + q_bytes) / (ms / 1e3) / 1e9 / world / hbm_peak},
         "knobs": {"tau": tau, "p": p, "lazy_fraction": args.lazy},
+        "sharding": f"sequence-sharded x{world} ({B} sequences on rank {rank})" if world > 1 else "single GPU",
     }
-    if not dense:
+    if not dense or world > 1:
+        cache.release()
         return res
     # dense full-cache decode baseline (flash-attn kv-cache kernel), same batch/context
     try:
         from flash_attn import flash_attn_with_kvcache
 
+        cache.release()
         del cache
         torch.cuda.empty_cache()
         kc = torch.randn(B, n, HKV, D, device="cuda", dtype=torch.bfloat16)
@@ -474,18 +498,21 @@ def run_ours(args):
                        "parallelism": f"head-sharded x{world}" if world > 1 else "single GPU",
                        "l2": "inputs larger than L2 (Q alone 470 MB at 64K); no flush"}}
     line["clocks"] = clk.summary()
+    b = int(res.selection.info[0])
+    line["selection"] = {"budget": b, "b_over_n": b / n, "flattest_group": int(res.selection.info[1]),
+                         "active_frac": float(res.active.float().mean())}
     if world > 1:
         multi_rank_sections(args, line, step, res, plan, Ql, Kl, Vl, O, nv, cfg, world, tc_peak, peak_src)
+        del res, Q, K, V, Ql, Kl, Vl, O
+        torch.cuda.empty_cache()
+        multi_rank_decode_train(args, line, world, rank, hbm_peak, plan)
     if rank != 0:
         if world > 1:
             dist.barrier()
             dist.destroy_process_group()
         return
 
-    b = int(res.selection.info[0])
     flops = work_flops(res, HKV) if world == 1 else None
-    line["selection"] = {"budget": b, "b_over_n": b / n, "flattest_group": int(res.selection.info[1]),
-                         "active_frac": float(res.active.float().mean())}
     if world == 1:
         line["selection"]["work_ratio_vs_dense_causal"] = flops / (4.0 * D * HQ * n * (n + 1) / 2)
         log("timed region done; per-kernel breakdown")
@@ -724,6 +751,48 @@ def multi_rank_sections(args, line, step, res, plan, Ql, Kl, Vl, O, nv, cfg, wor
                        "h2d_bytes_per_step": int(nb[0]), "d2h_bytes_per_step": int(nb[1]),
                        "api": "parallel.sparse_prefill_sharded per rank: pinned host shard in, host O rows out "
                               "(time: max over ranks; bytes: summed over ranks)"}
+
+
+def multi_rank_decode_train(args, line, world, rank, hbm_peak, plan):
+    """N > 1, every rank: C5 decode sequence-sharded (no collective) and the C4
+    training step head-sharded (parallel.sparse_attention_sharded: one
+    all_gather of block masses forward, one dK / dV all-reduce per split KV
+    group backward); step times are the max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    if not args.no_decode:
+        log("decode section (sequence-sharded)")
+        line["decode"] = decode_section(args, args.steps, args.warmup, hbm_peak, world=world, rank=rank)
+        torch.cuda.empty_cache()
+    if not args.no_train:
+        log("train section (head-sharded)")
+        from paper_2511_12201_b200.parallel import kv_grad_group, sparse_attention_sharded
+        from paper_2511_12201_b200.pipeline import SparsityConfig
+        from paper_2511_12201_b200.synthetic import generate_device
+
+        n = 32768
+        nv = n - N_TEXT
+        cfg = SparsityConfig(tau=args.tau, p=args.p)
+        kvg = kv_grad_group(HQ, HKV, world, rank)
+        Q, K, V = generate_device(HQ, HKV, D, nv, N_TEXT, seed=3, lazy_fraction=args.lazy)
+        Ql = Q[plan.q_start:plan.q_stop].clone().requires_grad_(True)
+        Kl, Vl = (x[plan.g_start:plan.g_stop].clone().requires_grad_(True) for x in (K, V))
+        dO = torch.randn_like(Ql)
+        del Q, K, V
+
+        def train_step():
+            O = sparse_attention_sharded(Ql, Kl, Vl, plan, nv, world, cfg, kv_group=kvg)
+            O.backward(dO)
+
+        train_step()
+        dist.barrier()
+        ms = time_cuda(train_step, max(3, args.steps // 2), 2)
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        line["train"] = {"workload": f"sparse attention fwd+bwd, {HQ}/{HKV} heads, d={D}, {n} tokens (C4), "
+                                     f"head-sharded x{world}", "ms_per_step": float(t),
+                         "tok_s": n / (float(t) / 1e3)}
 
 
 def run_reference(args):

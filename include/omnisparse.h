@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define OMNI_ABI_VERSION 1
+#define OMNI_ABI_VERSION 2
 
 enum omni_status {
   OMNI_OK = 0,
@@ -43,7 +43,10 @@ enum omni_status {
   OMNI_E_CUDA = 7                /* CUDA runtime failure                */
 };
 
-enum omni_dtype { OMNI_DTYPE_BF16 = 0, OMNI_DTYPE_F32 = 1 };
+/* F64 inputs are accepted by the selection-side entry points (K1, K2, K3x,
+ * gather): the reference's own precision, for drop-in callers holding
+ * float64 workloads. Attention (K4/K5/K7) is bf16. */
+enum omni_dtype { OMNI_DTYPE_BF16 = 0, OMNI_DTYPE_F32 = 1, OMNI_DTYPE_F64 = 2 };
 enum omni_granularity { OMNI_GRAN_TOKEN = 0, OMNI_GRAN_BLOCK = 1 };
 
 int omni_abi_version(void);
@@ -124,13 +127,45 @@ int omni_exact_mass(const void* Q, const void* K, int dtype, int n_q_heads, int 
  * budget_override > 0 skips the budget search (decode hand-off).
  * Outputs: selected i32 [Hkv, seq_len] (ascending, first b valid per group),
  * info i32 [4 + Hkv] = {budget, flattest, Hkv, nb, per-group counts...},
- * stats f64 [Hkv + 2] =
- * {kurtoses..., retained, total}; group_scores f64 [Hkv, nb] (nullable) =
- * per-token score of each block. Requires nb <= 8192.
- * Errors: PARAM for p outside (0, 1], nb too large, empty vision span.     */
+ * stats f64 [Hkv + 4] = {kurtoses..., retained, total, margin, replayed}:
+ * margin = distance of the budget decision from the threshold / total,
+ * replayed = 1.0 when that margin was inside the rounding bound and the
+ * reference's sequential cumsum decided; group_scores f64 [Hkv, nb] =
+ * per-token score of each block.
+ * Kurtosis is computed in NumPy's pairwise order and the budget is replayed
+ * in the reference's order whenever the fast scan could disagree with it, so
+ * for identical score vectors flattest group, budget and index sets equal the
+ * reference's bit for bit.
+ * workspace: omni_select_workspace() bytes (0 on the hot path: Hkv <= 8 and
+ * nb <= 1024; otherwise the general path needs it; seq_len <= 1,835,008).
+ * Errors: PARAM for p outside (0, 1], empty vision span, missing workspace. */
+size_t omni_select_workspace(int n_kv_heads, int seq_len, int block_size);
+int omni_select_ex(const double* block_mass, int n_q_heads, int n_kv_heads, int seq_len, int block_size, double p,
+                   int granularity, int vision_limit, int budget_override, int32_t* selected, int32_t* info,
+                   double* stats, double* group_scores, void* workspace, void* stream);
+/* omni_select: SURVEY §8b's name; omni_select_ex without a workspace.      */
 int omni_select(const double* block_mass, int n_q_heads, int n_kv_heads, int seq_len, int block_size, double p,
                 int granularity, int vision_limit, int budget_override, int32_t* selected, int32_t* info,
                 double* stats, double* group_scores, void* stream);
+
+/* Block sums of per-token score rows in np.add.reduceat order (first element
+ * + pairwise sum of the rest): x f64 [rows, n] -> out f64 [rows, nb]. The
+ * block mass of select_top_blocks (kv_select.py:160). */
+int omni_block_sums(const double* x, int rows, int n, int block_size, double* out, void* stream);
+
+/* select_top_blocks (kv_select.py:147-176) from given block masses: per
+ * group, blocks ranked by mass (ties to the lower block), whole blocks taken
+ * in rank order and the marginal block's lowest indices, exactly `budget`
+ * keys. block_mass f64 [G, nb]; selected i32 [G, seq_len] (ascending, first
+ * budget valid); info i32 [4 + G] (entries 4.. = per-group counts).
+ * workspace: omni_top_blocks_workspace() bytes.                           */
+size_t omni_top_blocks_workspace(int groups, int seq_len, int block_size);
+int omni_top_blocks(const double* block_mass, int groups, int seq_len, int block_size, int budget,
+                    int32_t* selected, int32_t* info, void* workspace, void* stream);
+
+/* The materialised BlockProbeMap (block_probe.py:60-63) from the workspace
+ * omni_probe_mass_map left: map f64 [Hq, nb, nb], zero above the diagonal. */
+int omni_probe_map(const void* workspace, int n_q_heads, int n_blocks, double* map, void* stream);
 
 /* ---------------------------------------------------------------- K6
  * Row gather / KV regrouping: dst[g, r, :] = src[g, idx[g, r], :] for
@@ -199,48 +234,47 @@ int omni_sparse_attn_bwd_ex(const void* Q, const void* K_sel, const void* V_sel,
                             void* workspace, void* stream);
 
 /* ---------------------------------------------------------------- K7
- * One slimmed decode step for a batch of sequences.
+ * One slimmed decode step for a batch of sequences over a PAGED slim cache.
  * Replaces classify_decode_query + _fetched_segments + decode_attention
  * (decode.py:124-194) under rule B: Q head h is classified (f64) against its
  * group's frozen probe keys (head 0 forced active when preserve_first_head);
  * a group's vision segment is read iff any of its Q heads is active; lazy Q
  * heads attend over text + answer only (exclusion semantics, decode.py:12-16).
- * q bf16 [B, Hq, d]; vision_k/v bf16 [B, Hkv, vcap, d] with vision_len i32
- * [B]; text_k/v bf16 [B, Hkv, n_text, d]; answer_k/v bf16 [B, Hkv, acap, d]
- * holding n_answer rows; k_lazy/k_act f64 [B, Hkv, d].
- * flags_override u8 [B, Hq] (nullable: the flags hook of decode.py:170-173).
- * Outputs: flags u8 [B, Hq]; out f32 [B, Hq, d].
- * Errors: DEGENERATE_CONTEXT when a lazy head has no text and no answer.   */
-size_t omni_decode_workspace(int batch, int n_q_heads, int vcap, int n_text, int acap, int head_dim);
-int omni_decode_step(const void* q, const void* vision_k, const void* vision_v, const int32_t* vision_len,
-                     const void* text_k, const void* text_v, int n_text, const void* answer_k, const void* answer_v,
-                     int n_answer, const double* k_lazy, const double* k_act, int batch, int n_q_heads,
-                     int n_kv_heads, int head_dim, int vcap, int acap, double tau, int preserve_first_head,
-                     const uint8_t* flags_override, uint8_t* flags, float* out, void* workspace, void* stream);
-
-/* K7 for a serving batch of ragged sequences: as omni_decode_step, but the
- * text and answer segment lengths are per sequence (device i32 [B]
- * text_len <= tcap, answer_len <= acap; text_k/v [B, Hkv, tcap, d]).
- * The reference keeps one growable list per head (decode.py:111-121); a
- * batch of sequences admitted at different times needs per-sequence lengths.
- * status i32 (device, required) receives this step's degenerate-context flag
- * (1: a lazy head had no text and no answer key, decode.py:152-153) without a
- * host synchronisation. Workspace: omni_decode_workspace(batch, Hq, vcap,
- * tcap, acap, d).                                                          */
-int omni_decode_step_varlen(const void* q, const void* vision_k, const void* vision_v, const int32_t* vision_len,
-                            const void* text_k, const void* text_v, const int32_t* text_len, int tcap,
-                            const void* answer_k, const void* answer_v, const int32_t* answer_len,
-                            const double* k_lazy, const double* k_act, int batch, int n_q_heads, int n_kv_heads,
-                            int head_dim, int vcap, int acap, double tau, int preserve_first_head,
-                            const uint8_t* flags_override, uint8_t* flags, float* out, void* workspace,
-                            int32_t* status, void* stream);
+ * Cache: pool_k / pool_v bf16 [n_pages, 64, 128]; table i32
+ * [B, Hkv, max_pages] lists each (sequence, group)'s pages: ceil(vision/64)
+ * vision pages, then ceil(text/64) text pages, then ceil(answer/64) answer
+ * pages; vision_len / text_len / answer_len i32 [B] rows per sequence.
+ * Rows are stored with 128 columns; head_dim <= 128 is the logical width
+ * (rows zero-padded past it) and sets the softmax scale 1 / sqrt(head_dim).
+ * n_chunks = max over sequences of ceil(pages / 32). q bf16 [B, Hq, 128];
+ * k_lazy / k_act f64 [B, Hkv, 128]; flags_override u8 [B, Hq] (nullable: the
+ * flags hook of decode.py:170-173). Outputs: flags u8 [B, Hq]; out f32
+ * [B, Hq, 128]; status i32 (device, required) = 1 when a lazy head had no
+ * text and no answer key (DegenerateContextError, decode.py:152-153),
+ * without a host synchronisation. workspace: omni_decode_workspace().       */
+size_t omni_decode_workspace(int batch, int n_q_heads, int n_chunks);
+int omni_decode(const void* q, const void* pool_k, const void* pool_v, int n_pages, const int32_t* table,
+                int max_pages, const int32_t* vision_len, const int32_t* text_len, const int32_t* answer_len,
+                int n_chunks, const double* k_lazy, const double* k_act, int batch, int n_q_heads, int n_kv_heads,
+                int head_dim, double tau, int preserve_first_head, const uint8_t* flags_override, uint8_t* flags,
+                float* out, void* workspace, int32_t* status, void* stream);
 
 /* append_answer (decode.py:111-121) for a batch in one launch: bf16 k/v_rows
- * [B, Hkv, d] go to answer_k/v [B, Hkv, acap, d] at row answer_len[s]
- * (device i32 [B], incremented; ragged batches) or n_answer (answer_len
- * NULL). The caller guarantees the row is below acap.                      */
-int omni_append_answer(const void* k_rows, const void* v_rows, void* answer_k, void* answer_v, int batch,
-                       int n_kv_heads, int head_dim, int acap, int n_answer, int32_t* answer_len, void* stream);
+ * [B, Hkv, 128] go to answer row answer_len[s] of every (sequence, group) —
+ * its page must already be in the table (the host allocates one every 64
+ * tokens) — and answer_len[s] advances on the device.                      */
+int omni_append_answer(const void* k_rows, const void* v_rows, void* pool_k, void* pool_v, const int32_t* table,
+                       int max_pages, const int32_t* vision_len, const int32_t* text_len, int32_t* answer_len,
+                       int batch, int n_kv_heads, int head_dim, void* stream);
+
+/* Rows into pages (cache building for the paged layout, K6): for group g <
+ * n_groups and r < count, the row src[g, idx ? idx[g, r] : r] ([G, src_rows,
+ * 128] bf16) goes to page table[g, first_slot + r / 64], row r % 64, of
+ * `pool`; the rest of the last page is zero-filled. `table` points at the
+ * sequence's [Hkv, max_pages] rows. The gather of build_cache
+ * (decode.py:92-107) straight into the serving pool.                      */
+int omni_page_write(const void* src, int n_groups, int src_rows, int head_dim, const int32_t* idx, int idx_stride,
+                    int count, const int32_t* table, int max_pages, int first_slot, void* pool, void* stream);
 
 /* classify_decode_query (decode.py:124-140) for a batch: q bf16 [B, Hq, d],
  * k_lazy / k_act f64 [B, Hkv, d] -> flags u8 [B, Hq] (float64 two-logit
@@ -249,12 +283,13 @@ int omni_decode_flags(const void* q, const double* k_lazy, const double* k_act, 
                       int n_kv_heads, int head_dim, double tau, int preserve_first_head, uint8_t* flags,
                       void* stream);
 
-/* omni_decode (SURVEY §8b's name for K7): identical to omni_decode_step.   */
-int omni_decode(const void* q, const void* vision_k, const void* vision_v, const int32_t* vision_len,
-                const void* text_k, const void* text_v, int n_text, const void* answer_k, const void* answer_v,
-                int n_answer, const double* k_lazy, const double* k_act, int batch, int n_q_heads, int n_kv_heads,
-                int head_dim, int vcap, int acap, double tau, int preserve_first_head,
-                const uint8_t* flags_override, uint8_t* flags, float* out, void* workspace, void* stream);
+/* classify_decode_query (decode.py:124-140) on float64 queries, the
+ * reference's precision (reference-signature operators): q f64
+ * [B, Hq, head_dim]; k_lazy / k_act f64 [B, Hkv, probe_stride] (the probe
+ * keys of a cache whose rows are zero-padded to probe_stride columns).     */
+int omni_decode_flags_f64(const double* q, const double* k_lazy, const double* k_act, int batch, int n_q_heads,
+                          int n_kv_heads, int head_dim, int probe_stride, double tau, int preserve_first_head,
+                          uint8_t* flags, void* stream);
 
 #ifdef __cplusplus
 }

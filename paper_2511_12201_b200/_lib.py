@@ -35,6 +35,13 @@ SIGNATURES = {
     "omni_exact_mass": (_c_int, [_p, _p, _c_int, _c_int, _c_int, _c_int, _c_int, _p, _p, _p]),
     "omni_select": (_c_int, [_p, _c_int, _c_int, _c_int, _c_int, _c_double, _c_int, _c_int, _c_int,
                              _p, _p, _p, _p, _p]),
+    "omni_select_workspace": (_c_size, [_c_int, _c_int, _c_int]),
+    "omni_select_ex": (_c_int, [_p, _c_int, _c_int, _c_int, _c_int, _c_double, _c_int, _c_int, _c_int,
+                                _p, _p, _p, _p, _p, _p]),
+    "omni_top_blocks_workspace": (_c_size, [_c_int, _c_int, _c_int]),
+    "omni_top_blocks": (_c_int, [_p, _c_int, _c_int, _c_int, _c_int, _p, _p, _p, _p]),
+    "omni_block_sums": (_c_int, [_p, _c_int, _c_int, _c_int, _p, _p]),
+    "omni_probe_map": (_c_int, [_p, _c_int, _c_int, _p, _p]),
     "omni_gather_rows": (_c_int, [_p, _c_int, _c_int, _c_int, _c_int, _p, _c_int, _p, _c_int, _p, _c_int,
                                   _c_int, _p]),
     "omni_scatter_rows": (_c_int, [_p, _c_int, _c_int, _c_int, _c_int, _p, _c_int, _p, _p, _c_int, _p]),
@@ -47,17 +54,15 @@ SIGNATURES = {
                                       _c_int, _p, _p, _p, _p, _p, _p]),
     "omni_sparse_attn_bwd_ex": (_c_int, [_p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _c_int, _c_int, _c_int, _c_int,
                                          _c_int, _c_int, _p, _p, _p, _p, _p, _p]),
-    "omni_decode_workspace": (_c_size, [_c_int, _c_int, _c_int, _c_int, _c_int, _c_int]),
-    "omni_decode_step": (_c_int, [_p, _p, _p, _p, _p, _p, _c_int, _p, _p, _c_int, _p, _p, _c_int, _c_int,
-                                  _c_int, _c_int, _c_int, _c_int, _c_double, _c_int, _p, _p, _p, _p, _p]),
-    "omni_decode": (_c_int, [_p, _p, _p, _p, _p, _p, _c_int, _p, _p, _c_int, _p, _p, _c_int, _c_int,
-                             _c_int, _c_int, _c_int, _c_int, _c_double, _c_int, _p, _p, _p, _p, _p]),
-    "omni_append_answer": (_c_int, [_p, _p, _p, _p, _c_int, _c_int, _c_int, _c_int, _c_int, _p, _p]),
+    "omni_decode_workspace": (_c_size, [_c_int, _c_int, _c_int]),
+    "omni_decode": (_c_int, [_p, _p, _p, _c_int, _p, _c_int, _p, _p, _p, _c_int, _p, _p, _c_int, _c_int, _c_int,
+                             _c_int, _c_double, _c_int, _p, _p, _p, _p, _p, _p]),
+    "omni_append_answer": (_c_int, [_p, _p, _p, _p, _p, _c_int, _p, _p, _p, _c_int, _c_int, _c_int, _p]),
+    "omni_page_write": (_c_int, [_p, _c_int, _c_int, _c_int, _p, _c_int, _c_int, _p, _c_int, _c_int, _p, _p]),
     "omni_decode_flags": (_c_int, [_p, _p, _p, _c_int, _c_int, _c_int, _c_int, _c_double, _c_int, _p, _p]),
+    "omni_decode_flags_f64": (_c_int, [_p, _p, _p, _c_int, _c_int, _c_int, _c_int, _c_int, _c_double, _c_int, _p,
+                                       _p]),
     "omni_slim_cache": (_c_int, [_p, _p, _c_int, _c_int, _c_int, _c_int, _p, _c_int, _c_int, _c_int, _p, _p, _p]),
-    "omni_decode_step_varlen": (_c_int, [_p, _p, _p, _p, _p, _p, _p, _c_int, _p, _p, _p, _p, _p, _c_int, _c_int,
-                                         _c_int, _c_int, _c_int, _c_int, _c_double, _c_int, _p, _p, _p, _p, _p,
-                                         _p]),
 }
 
 _lib = None
@@ -78,7 +83,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
-    if lib.omni_abi_version() != 1:
+    if lib.omni_abi_version() != 2:
         raise CudaError("libomnisparse ABI version mismatch")
     _lib = lib
     return lib

@@ -82,6 +82,15 @@ class AttentionWorkload:
     def seq_len(self) -> int:
         return _shape(self.queries[0])[0]
 
+    def source_dtype(self) -> torch.dtype:
+        """The device dtype that keeps the caller's precision for the
+        selection stages: the reference computes in float64, so
+        float64 workloads (the reference's own arrays) select in float64,
+        fp32 in fp32 and bf16 in bf16; attention always runs on bf16 copies."""
+        x = self.queries[0]
+        dt = x.dtype if isinstance(x, torch.Tensor) else torch.from_numpy(np.asarray(x)[:1]).dtype
+        return dt if dt in (torch.float64, torch.float32, torch.bfloat16) else torch.float32
+
     def device_tensors(self, dtype=torch.bfloat16, device="cuda"):
         """(Q [Hq,N,d], K [Hkv,N,d], V [Hkv,N,d]) on the GPU."""
         def pack(xs):

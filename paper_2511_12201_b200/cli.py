@@ -99,7 +99,7 @@ def run(argv=None) -> int:
         hkv = K.shape[0]
         vsel = ops.select(mass, hkv, a.nv + a.nt, cfg.block_size, cfg.p, "token", vision_limit=a.nv,
                           budget_override=b)
-        cache = gdec.build_cache(K, V, vsel.selected, b, a.nv, a.nt, k_lazy, k_act, a.heads,
+        cache = gdec.build_cache_device(K, V, vsel.selected, b, a.nv, a.nt, k_lazy, k_act, a.heads,
                                  answer_capacity=a.steps + 1)
         means = [unit_vision_mean(K, a.nv)]
         active_steps = total_steps = 0
@@ -107,11 +107,11 @@ def run(argv=None) -> int:
         gen.manual_seed(a.seed)
         for t in range(a.steps):
             q = decode_queries_device(a.heads, hkv, means, [a.seed], a.lazy_fraction, t)
-            _, flags = gdec.decode_attention(q, cache, cfg.tau)
+            _, flags = gdec.decode_attention_batch(q, cache, cfg.tau)
             fetched = flags.view(1, hkv, -1).any(dim=2)
             active_steps += int(fetched.sum())
             total_steps += hkv
-            gdec.append_answer(cache, torch.randn(1, hkv, a.dim, generator=gen, device="cuda"),
+            gdec.append_answer_batch(cache, torch.randn(1, hkv, a.dim, generator=gen, device="cuda"),
                                torch.randn(1, hkv, a.dim, generator=gen, device="cuda"))
         kv = gm.kv_reduction(a.nv, b, a.dim, active_steps, total_steps)
         rep = gm.MetricsReport(

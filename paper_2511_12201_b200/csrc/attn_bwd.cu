@@ -15,8 +15,10 @@
 //         dQ += dS K (TMEM accumulator);
 //   dkv   KV-tile CTAs looping over every Q tile of the group's Q heads that
 //         can see the tile: S^T = K Q^T, dP^T = V dO^T, P^T / dS^T -> smem,
-//         dV += P^T dO, dK += dS^T Q (TMEM accumulators). GQA accumulation over
-//         the group's Q heads happens inside one CTA (deterministic).
+//         dV += P^T dO, dK += dS^T Q (TMEM accumulators). One CTA per (key
+//         tile, Q head); the group's Q heads reduce into the zero-initialised
+//         fp32 dK / dV with vector atomics (red.global.add.v4.f32), so the
+//         fp32 summation order over a group's heads varies run to run.
 #include <math.h>
 #include <stdlib.h>
 #include <string.h>
@@ -1032,6 +1034,7 @@ extern "C" int omni_sparse_attn_bwd_ex(const void* Q, const void* K_sel, const v
                                        const int32_t* selected, const int32_t* sel_counts, int n_q_heads,
                                        int n_kv_heads, int seq_len, int head_dim, int cap, int dq_dtype, void* dQ,
                                        float* dK_sel, float* dV_sel, float* dV_sink, void* workspace, void* stream) {
+  omni_begin();
   OMNI_CHECK(dq_dtype == OMNI_DTYPE_F32 || dq_dtype == OMNI_DTYPE_BF16, OMNI_E_PARAM, "dQ must be f32 or bf16");
   OMNI_CHECK(head_dim == 128, OMNI_E_SHAPE, "sparse attention backward requires head_dim == 128");
   OMNI_CHECK(n_kv_heads >= 1 && n_q_heads % n_kv_heads == 0, OMNI_E_SHAPE, "n_q_heads must be a multiple of n_kv_heads");
@@ -1065,13 +1068,9 @@ extern "C" int omni_sparse_attn_bwd_ex(const void* Q, const void* K_sel, const v
   if ((rc = omni_make_tmap_rows(&tdo64, dOc, crow, 128, 2, 64, 64))) return rc;
   if ((rc = omni_make_tmap_rows(&tk, K_sel, (uint64_t)n_kv_heads * cap, 128, 2, 64, 128))) return rc;
   if ((rc = omni_make_tmap_rows(&tv, V_sel, (uint64_t)n_kv_heads * cap, 128, 2, 64, 128))) return rc;
-  static bool attr = false;
-  if (!attr) {
-    OMNI_CUDA_TRY(cudaFuncSetAttribute(bwd::dq_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bwd::dq::SMEM));
-    OMNI_CUDA_TRY(cudaFuncSetAttribute(bwd::dq_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bwd::dq::SMEM));
-    OMNI_CUDA_TRY(cudaFuncSetAttribute(bwd::dkv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bwd::dkv::SMEM));
-    attr = true;
-  }
+  OMNI_CUDA_TRY(omni_smem_attr(bwd::dq_kernel<0>, (int)bwd::dq::SMEM));
+  OMNI_CUDA_TRY(omni_smem_attr(bwd::dq_kernel<1>, (int)bwd::dq::SMEM));
+  OMNI_CUDA_TRY(omni_smem_attr(bwd::dkv_kernel, (int)bwd::dkv::SMEM));
   const int n_tiles = capq / 128;
   static const int dq_probe = [] {
     const char* e = getenv("OMNI_DQ_PROBE");
@@ -1100,11 +1099,7 @@ extern "C" int omni_sparse_attn_bwd_ex(const void* Q, const void* K_sel, const v
                 : probe == 2 ? bwd::dkv2_kernel<2>
                 : probe == 3 ? bwd::dkv2_kernel<3>
                              : bwd::dkv2_kernel<0>;
-    static bool attr2 = false;
-    if (!attr2) {
-      OMNI_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bwd::dkv2::SMEM));
-      attr2 = true;
-    }
+    OMNI_CUDA_TRY(omni_smem_attr(kern, (int)bwd::dkv2::SMEM));
     kern<<<dim3(cap / 128, n_kv_heads * rep), bwd::dkv2::NTHREADS, bwd::dkv2::SMEM, st>>>(
         tq128, tdo128, tk, tv, rows, counts, selected, sel_counts, lse2c, Dc, visc, rep, seq_len, cap, capq, dK_sel,
         dV_sel);
@@ -1115,6 +1110,7 @@ extern "C" int omni_sparse_attn_bwd_ex(const void* Q, const void* K_sel, const v
 // Profiling support (OMNI_BWD_PROBE=3): copies the 8 dkv phase-cycle sums to
 // host memory and resets them.
 extern "C" int omni_debug_bwd_trace(unsigned long long* host8) {
+  omni_begin();
   OMNI_CUDA_TRY(cudaMemcpyFromSymbol(host8, bwd::g_bwd_trace, sizeof(unsigned long long) * 8));
   unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   OMNI_CUDA_TRY(cudaMemcpyToSymbol(bwd::g_bwd_trace, z, sizeof(z)));
@@ -1126,6 +1122,7 @@ extern "C" int omni_sparse_attn_bwd(const void* Q, const void* K_sel, const void
                                     const int32_t* selected, const int32_t* sel_counts, int n_q_heads, int n_kv_heads,
                                     int seq_len, int head_dim, int cap, float* dQ, float* dK_sel, float* dV_sel,
                                     float* dV_sink, void* workspace, void* stream) {
+  omni_begin();
   return omni_sparse_attn_bwd_ex(Q, K_sel, V_sel, O, dO, lse, rows, counts, selected, sel_counts, n_q_heads,
                                  n_kv_heads, seq_len, head_dim, cap, OMNI_DTYPE_F32, dQ, dK_sel, dV_sel, dV_sink,
                                  workspace, stream);

@@ -591,6 +591,7 @@ extern "C" int omni_sparse_attn_fwd_ex(const void* Q, const void* K_sel, const v
                                        const int32_t* sel_counts, int n_q_heads, int n_kv_heads, int seq_len,
                                        int head_dim, int cap, int sink_index, void* O, float* lse, int32_t* status,
                                        void* stream) {
+  omni_begin();
   OMNI_CHECK(head_dim == 128, OMNI_E_SHAPE, "sparse attention kernel requires head_dim == 128");
   OMNI_CHECK(n_kv_heads >= 1 && n_q_heads % n_kv_heads == 0, OMNI_E_SHAPE, "n_q_heads must be a multiple of n_kv_heads");
   OMNI_CHECK(cap >= 128 && cap % 128 == 0, OMNI_E_SHAPE, "cap must be a positive multiple of 128");
@@ -649,15 +650,10 @@ extern "C" int omni_sparse_attn_fwd_ex(const void* Q, const void* K_sel, const v
             : poly == 6 ? fwd::sparse_fwd_kernel<6, false, false, true>
                         : fwd::sparse_fwd_kernel<4, false, false, true>;
   const bool use_fast = status != nullptr && fast_env && !trace && poly >= 0;
-  static bool attr_set[2] = {false, false};
-  if (!attr_set[0]) {
-    OMNI_CUDA_TRY(cudaFuncSetAttribute(safe, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fwd::SMEM_BYTES));
-    attr_set[0] = true;
-  }
-  if (use_fast && !attr_set[1]) {
-    OMNI_CUDA_TRY(cudaFuncSetAttribute(fast, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fwd::SMEM_BYTES));
-    OMNI_CUDA_TRY(cudaFuncSetAttribute(redo, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fwd::SMEM_BYTES));
-    attr_set[1] = true;
+  OMNI_CUDA_TRY(omni_smem_attr(safe, (int)fwd::SMEM_BYTES));
+  if (use_fast) {
+    OMNI_CUDA_TRY(omni_smem_attr(fast, (int)fwd::SMEM_BYTES));
+    OMNI_CUDA_TRY(omni_smem_attr(redo, (int)fwd::SMEM_BYTES));
   }
   const int n_tiles = (seq_len + 2 * fwd::BM - 1) / (2 * fwd::BM);
   dim3 grid(n_tiles * n_q_heads);
@@ -689,6 +685,7 @@ extern "C" int omni_sparse_attn_fwd(const void* Q, const void* K_sel, const void
                                     const int32_t* rows, const int32_t* counts, const int32_t* selected,
                                     const int32_t* sel_counts, int n_q_heads, int n_kv_heads, int seq_len,
                                     int head_dim, int cap, int sink_index, void* O, float* lse, void* stream) {
+  omni_begin();
   return omni_sparse_attn_fwd_ex(Q, K_sel, V_sel, V, rows, counts, selected, sel_counts, n_q_heads, n_kv_heads,
                                  seq_len, head_dim, cap, sink_index, O, lse, nullptr, stream);
 }
@@ -696,6 +693,7 @@ extern "C" int omni_sparse_attn_fwd(const void* Q, const void* K_sel, const void
 // Profiling support (OMNI_FWD_TRACE=1): copies the 8 per-phase cycle sums
 // of the traced K4 launches to host memory and resets them.
 extern "C" int omni_debug_fwd_trace(unsigned long long* host8) {
+  omni_begin();
   OMNI_CUDA_TRY(cudaMemcpyFromSymbol(host8, fwd::g_fwd_trace, sizeof(unsigned long long) * 8));
   unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   OMNI_CUDA_TRY(cudaMemcpyToSymbol(fwd::g_fwd_trace, z, sizeof(z)));

@@ -462,7 +462,7 @@ int omni_sparse_attn_fwd_pair(const void* Q, const void* K_sel, const void* V_se
             : poly == 6 ? fwd2::sparse_fwd_pair_kernel<6>
             : poly == 8 ? fwd2::sparse_fwd_pair_kernel<8>
                         : fwd2::sparse_fwd_pair_kernel<4>;
-  OMNI_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fwd2::SMEM_BYTES));
+  OMNI_CUDA_TRY(omni_smem_attr(kern, (int)fwd2::SMEM_BYTES));
   const int n_pairs = (seq_len + 2 * fwd2::BM - 1) / (2 * fwd2::BM);
   dim3 grid(2 * n_pairs * n_q_heads);
   kern<<<grid, fwd2::NTHREADS, fwd2::SMEM_BYTES, stream>>>(
@@ -473,6 +473,7 @@ int omni_sparse_attn_fwd_pair(const void* Q, const void* K_sel, const void* V_se
 }
 
 extern "C" int omni_debug_fwd_pair_trace(unsigned long long* host8) {
+  omni_begin();
   OMNI_CUDA_TRY(cudaMemcpyFromSymbol(host8, fwd2::g_trace, sizeof(unsigned long long) * 8));
   unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   OMNI_CUDA_TRY(cudaMemcpyToSymbol(fwd2::g_trace, z, sizeof(z)));

@@ -4,6 +4,8 @@
 #include <string.h>
 
 #include <mutex>
+#include <map>
+#include <utility>
 
 #include "common.cuh"
 
@@ -14,11 +16,33 @@ void omni_set_last_error(const char* msg) {
   g_last_error[sizeof(g_last_error) - 1] = '\0';
 }
 
+void omni_set_cuda_error(const char* what, cudaError_t e) {
+  snprintf(g_last_error, sizeof(g_last_error), "%s: %s", what, cudaGetErrorString(e));
+}
+
+cudaError_t omni_smem_attr_raw(const void* fn, int bytes) {
+  // the attribute only ever grows per (kernel, device): a later, smaller
+  // request must not lower the limit a concurrent or later launch relies on
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, int> cur;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const auto key = std::make_pair(fn, dev);
+  std::lock_guard<std::mutex> lock(mu);
+  const auto it = cur.find(key);
+  if (it != cur.end() && it->second >= bytes) return cudaSuccess;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) cur[key] = bytes;
+  return e;
+}
+
 extern "C" int omni_abi_version(void) { return OMNI_ABI_VERSION; }
 
 extern "C" const char* omni_last_error(void) { return g_last_error; }
 
 extern "C" int omni_device_check(void) {
+  omni_begin();
   int dev = 0;
   OMNI_CUDA_TRY(cudaGetDevice(&dev));
   cudaDeviceProp prop;

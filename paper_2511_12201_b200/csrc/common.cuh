@@ -26,7 +26,7 @@
   do {                                                        \
     cudaError_t _e = (expr);                                  \
     if (_e != cudaSuccess) {                                  \
-      omni_set_last_error(cudaGetErrorString(_e));            \
+      omni_set_cuda_error(#expr, _e);                         \
       return OMNI_E_CUDA;                                     \
     }                                                         \
   } while (0)
@@ -41,11 +41,27 @@
 
 // Defined in capi.cu: thread-local last-error string for diagnostics.
 void omni_set_last_error(const char* msg);
+void omni_set_cuda_error(const char* what, cudaError_t e);  // "<what>: <CUDA error string>"
+
+// Every C-ABI entry point starts here: clears a non-sticky error another
+// runtime call of this thread left behind (torch, CUB dispatch), so the
+// launch check after our own launches reports only our launches.
+static inline void omni_begin() { (void)cudaGetLastError(); }
+
+// Defined in capi.cu: raises the dynamic shared-memory limit of kernel `fn`
+// to at least `bytes` on the CURRENT device (the limit only grows); the
+// attribute is per device context, so a process driving two GPUs sets it on
+// each. Thread-safe.
+cudaError_t omni_smem_attr_raw(const void* fn, int bytes);
+template <typename F>
+static inline cudaError_t omni_smem_attr(F* fn, int bytes) {
+  return omni_smem_attr_raw(reinterpret_cast<const void*>(fn), bytes);
+}
 
 static inline int omni_launch_check() {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
-    omni_set_last_error(cudaGetErrorString(e));
+    omni_set_cuda_error("kernel launch", e);
     return OMNI_E_CUDA;
   }
   return OMNI_OK;
@@ -63,6 +79,8 @@ template <typename T>
 __device__ __forceinline__ double to_f64(T x);
 template <>
 __device__ __forceinline__ double to_f64<float>(float x) { return static_cast<double>(x); }
+template <>
+__device__ __forceinline__ double to_f64<double>(double x) { return x; }
 template <>
 __device__ __forceinline__ double to_f64<__nv_bfloat16>(__nv_bfloat16 x) {
   return static_cast<double>(__bfloat162float(x));

@@ -1,24 +1,29 @@
-// K7: slimmed decode attention over the slim cache (split-K flash decoding).
+// K7: slimmed decode attention over a PAGED slim cache (split-K flash decoding).
 //
 // Replaces classify_decode_query + _fetched_segments + decode_attention
 // (decode.py:124-194) for a batch of sequences under GQA rule B.
 //
-//   decode_flags_kernel   one warp per (sequence, Q head): float64
-//                         two-logit classification against the frozen probe
-//                         keys (query_select.py:63-68), head 0 forced active.
-//   decode_partial_kernel CTA = (2048-key chunk, KV group, sequence), 4 warps x
-//                         512 keys. A group's key list is [vision (only if any
-//                         of its Q heads is active — the fetch skip of
-//                         decode.py:176-190), text, answer]; lazy Q heads see
-//                         -inf on vision keys (exclusion, decode.py:12-16).
-//                         The group's <= 16 Q heads form the M=16 rows of
-//                         mma.sync.m16n8k16 tiles, so each K / V row is read
-//                         from HBM exactly once and feeds every head. Head-dim
-//                         and key orders inside a tile are permuted so every
-//                         lane issues contiguous 16-byte loads straight into
-//                         MMA fragments (no shared-memory staging).
+// Cache layout (serving): one pool of 64-row pages per
+// layer, K and V each [P, 64, 128] bf16. Sequence slot s, KV group g owns the
+// page list table[(s * Hkv + g) * max_pages + j]: ceil(b / 64) vision pages,
+// then ceil(n_text / 64) text pages, then ceil(n_answer / 64) answer pages
+// (the segment order of _fetched_segments, decode.py:143-154). Admitting a
+// sequence writes only its own pages, evicting one returns its pages, growing
+// an answer takes a page every 64 tokens: no operation copies other
+// sequences' KV (the reference grows one Python list per head,
+// decode.py:111-121).
+//
+//   decode_partial_tma_kernel  persistent CTAs over (32-page chunk, KV group,
+//       sequence) items. A producer warp classifies the item's Q heads
+//       (float64 two-logit rule against the frozen probe keys, head 0 forced
+//       active) and streams its pages with SWIZZLE_128B TMA (one 64-row box
+//       per page and half-row) into a 4-stage ring; a group's vision pages
+//       are skipped when all its Q heads are lazy (the fetch skip of
+//       decode.py:176-190), lazy heads see -inf on vision keys (exclusion,
+//       decode.py:12-16). Four consumer warps: the group's <= 8 Q heads as the
+//       M rows of mma.sync m16n8k16 (ldmatrix B fragments), online softmax.
 //   decode_combine_kernel merges the per-chunk (max, sum, acc) partials.
-// HBM-bound: bytes = fetched vision + text + answer K/V rows, once each.
+// HBM-bound: bytes = fetched vision + text + answer pages, once each.
 #include <math.h>
 #include <stdlib.h>
 #include <string.h>
@@ -29,20 +34,21 @@ namespace omni {
 namespace dec {
 
 constexpr int D = 128;
-constexpr int WARP_KEYS = 512;
-constexpr int CTA_KEYS = 4 * WARP_KEYS;
+constexpr int PAGE = 64;                       // rows per page = TMA box rows = keys per tile
+constexpr int CHUNK_PAGES = 32;                // pages per work item (2048 keys)
 constexpr int MAXREP = 8;  // rows of the m16 tile used (rows 8..15 stay zero)
 
-// Text / answer segment lengths: one value for the whole batch, or per
-// sequence (serving batches of ragged prompts and answers). The text segment
-// of (sequence s, group g) starts at row (s * Hkv + g) * tcap.
-struct SegLens {
-  const int32_t* tlen;  // nullable: per-sequence text lengths
-  const int32_t* alen;  // nullable: per-sequence answer lengths
-  int nt, na, tcap;
-  __device__ __forceinline__ int text(int s) const { return tlen ? tlen[s] : nt; }
-  __device__ __forceinline__ int answer(int s) const { return alen ? alen[s] : na; }
+// Per-sequence lengths (device i32 [B], rows) and the page table.
+struct Paged {
+  const int32_t* table;  // [B, Hkv, max_pages]
+  int max_pages;
+  const int32_t* vlen;   // vision rows (= budget b)
+  const int32_t* tlen;   // text rows
+  const int32_t* alen;   // answer rows
+  double scale;          // 1 / sqrt(head_dim); rows stored with D columns (zero-padded past head_dim)
 };
+
+__device__ __forceinline__ int pages_of(int rows) { return (rows + PAGE - 1) / PAGE; }
 
 __device__ __forceinline__ void mma_bf16_16816(float* c, const uint32_t* a, uint32_t b0, uint32_t b1) {
   asm volatile(
@@ -61,7 +67,7 @@ __device__ __forceinline__ void mma_bf16_16816(float* c, const uint32_t* a, uint
 __device__ __forceinline__ uint32_t group_flag_mask(const __nv_bfloat16* __restrict__ q,
                                                     const double* __restrict__ k_lazy,
                                                     const double* __restrict__ k_act, int s, int g, int Hq, int Hkv,
-                                                    double tau, int preserve,
+                                                    double tau, double scale, int preserve,
                                                     const uint8_t* __restrict__ flags_override, double* sk) {
   // sk: 2 x D doubles of shared memory owned by this warp (the group's probe
   // keys, staged with coalesced loads so the float64 dot chains read them at
@@ -103,7 +109,6 @@ __device__ __forceinline__ uint32_t group_flag_mask(const __nv_bfloat16* __restr
     da += __shfl_xor_sync(0xffffffffu, da, 1);
     dl += __shfl_xor_sync(0xffffffffu, dl, 2);
     da += __shfl_xor_sync(0xffffffffu, da, 2);
-    const double scale = 1.0 / sqrt(static_cast<double>(D));
     const double l0 = dl * scale, l1 = da * scale, mx = fmax(l0, l1);
     const double e0 = exp(l0 - mx), e1 = exp(l1 - mx);
     f = (r < rep && e1 / (e0 + e1) > tau) ? 1 : 0;
@@ -117,200 +122,13 @@ __device__ __forceinline__ uint32_t group_flag_mask(const __nv_bfloat16* __restr
 }
 
 __global__ void decode_flags_kernel(const __nv_bfloat16* __restrict__ q, const double* __restrict__ k_lazy,
-                                    const double* __restrict__ k_act, int Hq, int Hkv, double tau, int preserve,
+                                    const double* __restrict__ k_act, int Hq, int Hkv, double tau, double scale,
+                                    int preserve,
                                     const uint8_t* __restrict__ flags_override, uint8_t* __restrict__ flags) {
   __shared__ __align__(16) double sk[2 * D];
   const int g = blockIdx.x, s = blockIdx.y, lane = threadIdx.x, rep = Hq / Hkv;
-  const uint32_t mask = group_flag_mask(q, k_lazy, k_act, s, g, Hq, Hkv, tau, preserve, flags_override, sk);
+  const uint32_t mask = group_flag_mask(q, k_lazy, k_act, s, g, Hq, Hkv, tau, scale, preserve, flags_override, sk);
   if (lane < rep) flags[(size_t)s * Hq + g * rep + lane] = static_cast<uint8_t>((mask >> lane) & 1u);
-}
-
-__global__ void __launch_bounds__(128) decode_partial_kernel(
-    const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ vk, const __nv_bfloat16* __restrict__ vv,
-    const int32_t* __restrict__ vlen, const __nv_bfloat16* __restrict__ tk, const __nv_bfloat16* __restrict__ tv,
-    const __nv_bfloat16* __restrict__ ak, const __nv_bfloat16* __restrict__ av, SegLens sl, int Hq, int Hkv,
-    int vcap, int acap, const uint8_t* __restrict__ flags, float* __restrict__ part_ml, float* __restrict__ part_acc,
-    int n_chunks, int* __restrict__ degenerate) {
-  __shared__ float s_ml[4][MAXREP][2];
-  if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && threadIdx.x == 0) *degenerate = 0;  // for the merge
-  __shared__ float s_acc[4][MAXREP][D];
-  const int c = blockIdx.x, g = blockIdx.y, s = blockIdx.z;
-  const int rep = Hq / Hkv;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int r4 = lane & 3, gid = lane >> 2;  // thread-in-group, group id (row / key / column index)
-
-  // per-row (Q head) vision visibility; row gid (< rep) is this thread's A/C row
-  int any = 0;
-  for (int r = 0; r < rep; ++r) any |= flags[(size_t)s * Hq + g * rep + r];
-  const bool row_valid = gid < rep;
-  const bool row_vis = row_valid && flags[(size_t)s * Hq + g * rep + (row_valid ? gid : 0)];
-  const int vl = vlen[s], nt = sl.text(s), tcap = sl.tcap;
-  const int k_start = any ? 0 : vl;       // skip the vision segment when every head is lazy
-  const int k_end = vl + nt + sl.answer(s);
-  const int w0 = k_start + c * CTA_KEYS + warp * WARP_KEYS;
-  const int w1 = min(k_end, w0 + WARP_KEYS);
-
-  // Q A-fragments with the head-dim permutation: lane r4 owns dims r4*32 .. +31;
-  // k-step ks uses dims r4*32 + ks*4 + {0,1} (a0a1) and {2,3} (a4a5).
-  uint32_t qa[8][4];
-  {
-    uint4 qv[4];
-    const uint4* qrow = reinterpret_cast<const uint4*>(q + ((size_t)s * Hq + g * rep + (row_valid ? gid : 0)) * D) + r4 * 4;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) qv[i] = row_valid ? __ldg(qrow + i) : make_uint4(0, 0, 0, 0);
-    const uint32_t* qw = reinterpret_cast<const uint32_t*>(qv);
-#pragma unroll
-    for (int ks = 0; ks < 8; ++ks) {
-      qa[ks][0] = qw[2 * ks];      // row gid, dims +0,+1
-      qa[ks][1] = 0u;              // row gid+8 (padding)
-      qa[ks][2] = qw[2 * ks + 1];  // row gid, dims +2,+3
-      qa[ks][3] = 0u;
-    }
-  }
-  const float sl2 = static_cast<float>(kLog2e / sqrt(static_cast<double>(D)));
-  float m_run = -INFINITY, l_run = 0.f;
-  float acc[16][4];
-#pragma unroll
-  for (int i = 0; i < 16; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
-
-  const size_t sg = (size_t)s * Hkv + g;
-  auto krow = [&](int v) -> const uint4* {
-    const __nv_bfloat16* p;
-    if (v < vl) p = vk + (sg * vcap + v) * D;
-    else if (v < vl + nt) p = tk + (sg * tcap + (v - vl)) * D;
-    else p = ak + (sg * acap + (v - vl - nt)) * D;
-    return reinterpret_cast<const uint4*>(p);
-  };
-  auto vrow = [&](int v) -> const uint4* {
-    const __nv_bfloat16* p;
-    if (v < vl) p = vv + (sg * vcap + v) * D;
-    else if (v < vl + nt) p = tv + (sg * tcap + (v - vl)) * D;
-    else p = av + (sg * acap + (v - vl - nt)) * D;
-    return reinterpret_cast<const uint4*>(p);
-  };
-
-  for (int kb = w0; kb < w1; kb += 16) {
-    // ---- K fragments: n-tile t covers keys kb + 8t + gid; lane loads dims r4*32 .. +31
-    uint4 kf[2][4];
-    bool kvalid[2];
-#pragma unroll
-    for (int t = 0; t < 2; ++t) {
-      const int key = kb + 8 * t + gid;
-      kvalid[t] = key < w1;
-      const uint4* p = krow(kvalid[t] ? key : kb) + r4 * 4;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) kf[t][i] = __ldg(p + i);
-    }
-    // ---- V rows for the B fragments of P V: keys kb + 2*r4 + {0,1,8,9}, dims gid*16 .. +15
-    uint4 vf[4][2];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int key = kb + 2 * r4 + (u & 1) + 8 * (u >> 1);
-      const uint4* p = vrow(key < w1 ? key : kb) + gid * 2;
-      vf[u][0] = __ldg(p);
-      vf[u][1] = __ldg(p + 1);
-    }
-    // ---- S = Q K^T (rows = heads, cols = 16 keys)
-    float sc[2][4];
-#pragma unroll
-    for (int t = 0; t < 2; ++t) {
-      sc[t][0] = sc[t][1] = sc[t][2] = sc[t][3] = 0.f;
-      const uint32_t* kw = reinterpret_cast<const uint32_t*>(kf[t]);
-#pragma unroll
-      for (int ks = 0; ks < 8; ++ks) mma_bf16_16816(sc[t], qa[ks], kw[2 * ks], kw[2 * ks + 1]);
-    }
-    // ---- mask (keys beyond the range; vision keys for lazy heads) and online softmax
-    float x[4];
-#pragma unroll
-    for (int t = 0; t < 2; ++t) {
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int key = kb + 8 * t + 2 * r4 + e;  // C fragment column of this thread
-        const bool ok = row_valid && key < w1 && (key >= vl || row_vis);
-        x[2 * t + e] = ok ? sc[t][e] * sl2 : -INFINITY;
-      }
-    }
-    float mt = fmaxf(fmaxf(x[0], x[1]), fmaxf(x[2], x[3]));
-    mt = fmaxf(mt, __shfl_xor_sync(0xffffffffu, mt, 1));
-    mt = fmaxf(mt, __shfl_xor_sync(0xffffffffu, mt, 2));
-    const float m_new = fmaxf(m_run, mt);
-    if (m_new > m_run + 8.0f) {  // lazy rescale of this row's accumulator
-      const float alpha = (m_run == -INFINITY) ? 0.f : fast_exp2(m_run - m_new);
-      l_run *= alpha;
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        acc[i][0] *= alpha;
-        acc[i][1] *= alpha;
-      }
-      m_run = m_new;
-    }
-    const float mu = (m_run == -INFINITY) ? 0.f : m_run;
-    float p[4];
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      p[e] = fast_exp2(x[e] - mu);
-      l_run += p[e];
-    }
-    // P as the A fragment: a0a1 = keys 2r4,+1 (n-tile 0), a4a5 = keys 8+2r4,+1 (n-tile 1)
-    uint32_t pa[4] = {pack_bf16x2(p[0], p[1]), 0u, pack_bf16x2(p[2], p[3]), 0u};
-    // ---- O += P V over 16 d n-tiles; n-tile nt, column gid <-> dim gid*16 + nt
-#pragma unroll
-    for (int ntl = 0; ntl < 16; ++ntl) {
-      const int w = ntl >> 1, hi = ntl & 1;
-      const uint32_t* v0 = reinterpret_cast<const uint32_t*>(&vf[0][w >> 2]);
-      const uint32_t* v1 = reinterpret_cast<const uint32_t*>(&vf[1][w >> 2]);
-      const uint32_t* v2 = reinterpret_cast<const uint32_t*>(&vf[2][w >> 2]);
-      const uint32_t* v3 = reinterpret_cast<const uint32_t*>(&vf[3][w >> 2]);
-      const int wi = w & 3;
-      const uint32_t sel = hi ? 0x7632u : 0x5410u;
-      const uint32_t b0 = __byte_perm(v0[wi], v1[wi], sel);
-      const uint32_t b1 = __byte_perm(v2[wi], v3[wi], sel);
-      float* cc = acc[ntl];
-      asm volatile(
-          "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-          "{%0,%1,%2,%3};"
-          : "+f"(cc[0]), "+f"(cc[1]), "+f"(cc[2]), "+f"(cc[3])
-          : "r"(pa[0]), "r"(pa[1]), "r"(pa[2]), "r"(pa[3]), "r"(b0), "r"(b1));
-    }
-  }
-  // ---- per-warp row results -> smem; row gid's l is spread over the 4 lanes of its group
-  l_run += __shfl_xor_sync(0xffffffffu, l_run, 1);
-  l_run += __shfl_xor_sync(0xffffffffu, l_run, 2);
-  if (row_valid) {
-    if (r4 == 0) {
-      s_ml[warp][gid][0] = m_run;
-      s_ml[warp][gid][1] = l_run;
-    }
-    // C fragment: acc[nt][0/1] = O[row gid][n = 2*r4 + {0,1}] -> dim n*16 + nt
-#pragma unroll
-    for (int ntl = 0; ntl < 16; ++ntl) {
-      s_acc[warp][gid][(2 * r4) * 16 + ntl] = acc[ntl][0];
-      s_acc[warp][gid][(2 * r4 + 1) * 16 + ntl] = acc[ntl][1];
-    }
-  }
-  __syncthreads();
-  // ---- combine the 4 warps, write this chunk's partial per Q head
-  for (int e = threadIdx.x; e < rep * D; e += blockDim.x) {
-    const int r = e / D, col = e % D;
-    float M = -INFINITY;
-#pragma unroll
-    for (int w = 0; w < 4; ++w) M = fmaxf(M, s_ml[w][r][0]);
-    float L = 0.f, o = 0.f;
-#pragma unroll
-    for (int w = 0; w < 4; ++w) {
-      const float m = s_ml[w][r][0];
-      if (m == -INFINITY) continue;
-      const float wt = fast_exp2(m - M);
-      L += wt * s_ml[w][r][1];
-      o += wt * s_acc[w][r][col];
-    }
-    const size_t base = ((size_t)s * Hq + g * rep + r) * n_chunks + c;
-    part_acc[base * D + col] = o;
-    if (col == 0) {
-      part_ml[base * 2 + 0] = M;
-      part_ml[base * 2 + 1] = L;
-    }
-  }
 }
 
 __global__ void decode_combine_kernel(const float* __restrict__ part_ml, const float* __restrict__ part_acc,
@@ -340,18 +158,8 @@ __global__ void decode_combine_kernel(const float* __restrict__ part_ml, const f
   }
 }
 
-// ---------------------------------------------------------------- K7 v3
-// TMA-staged variant (default): persistent CTAs (one per SM) walk the
-// (chunk, KV group, sequence) work items; a producer warp streams 64-key K and
-// V tiles of each segment (vision / text / answer, 2-D tensor maps with
-// SWIZZLE_128B) into an NSTG-stage shared-memory ring that runs ahead across
-// work items, so each SM keeps up to NSTG x 32 KB of HBM reads in flight with
-// no register staging. Four consumer warps take 16 keys of each tile: B
-// fragments of S = Q K^T come from ldmatrix.x4 and of O += P V from
-// ldmatrix.x4.trans (conflict-free on the swizzled tiles), the MMA and softmax
-// math is that of decode_partial_kernel.
-constexpr int TK = 64, NSTG = 4, NCW = 4;
-constexpr uint32_t TATOM = TK * 128;      // 64 rows x 128 B
+constexpr int NSTG = 4, NCW = 4;
+constexpr uint32_t TATOM = PAGE * 128;    // 64 rows x 128 B
 constexpr uint32_t TTILE = 2 * TATOM;     // 64 keys x 128 d bf16 = 16 KB
 constexpr uint32_t TSTAGE = 2 * TTILE;    // K + V
 constexpr uint32_t TSMEM = NSTG * TSTAGE + 1024;
@@ -372,63 +180,38 @@ __device__ __forceinline__ uint32_t toff(int r, int c) {
 }
 
 struct DecItem {
-  int s, g, c, lo, hi, vl, nt, any;
+  int s, g, c, t0, t1, tv, tt, vl, nt, na;
 };
 
-__device__ __forceinline__ DecItem dec_item(int t, int nc, int Hq, int Hkv, const SegLens& sl,
-                                            const int32_t* __restrict__ vlen, const uint8_t* __restrict__ flags) {
+// Item t = (chunk c, group g, sequence s): page slots [t0, t1) of the group's
+// page list, the vision pages skipped when no Q head of the group is active.
+__device__ __forceinline__ DecItem dec_item(int t, int nc, int Hkv, const Paged& pg, uint32_t mask) {
   DecItem it;
   it.c = t % nc;
   it.g = (t / nc) % Hkv;
   it.s = t / (nc * Hkv);
-  const int rep = Hq / Hkv;
-  int any = 0;
-  for (int r = 0; r < rep; ++r) any |= flags[(size_t)it.s * Hq + it.g * rep + r];
-  it.any = any;
-  it.vl = vlen[it.s];
-  it.nt = sl.text(it.s);
-  const int k_start = any ? 0 : it.vl;  // skip the vision segment when every head is lazy
-  const int k_end = it.vl + it.nt + sl.answer(it.s);
-  it.lo = k_start + it.c * CTA_KEYS;
-  it.hi = min(k_end, it.lo + CTA_KEYS);
+  it.vl = pg.vlen[it.s];
+  it.nt = pg.tlen[it.s];
+  it.na = pg.alen[it.s];
+  it.tv = pages_of(it.vl);
+  it.tt = pages_of(it.nt);
+  const int first = mask ? 0 : it.tv;
+  const int end = it.tv + it.tt + pages_of(it.na);
+  it.t0 = first + it.c * CHUNK_PAGES;
+  it.t1 = min(end, it.t0 + CHUNK_PAGES);
   return it;
 }
 
-// FUSED: the item's key range from the group's active mask (computed by the
-// producer warp, handed to the consumers through a shared-memory ring)
-__device__ __forceinline__ DecItem dec_item_mask(int t, int nc, int Hkv, const SegLens& sl,
-                                                 const int32_t* __restrict__ vlen, uint32_t mask) {
-  DecItem it;
-  it.c = t % nc;
-  it.g = (t / nc) % Hkv;
-  it.s = t / (nc * Hkv);
-  it.any = mask != 0u;
-  it.vl = vlen[it.s];
-  it.nt = sl.text(it.s);
-  const int k_start = it.any ? 0 : it.vl;
-  const int k_end = it.vl + it.nt + sl.answer(it.s);
-  it.lo = k_start + it.c * CTA_KEYS;
-  it.hi = min(k_end, it.lo + CTA_KEYS);
-  return it;
+// page slot j of item `it`: segment (0 vision, 1 text, 2 answer) and valid rows
+__device__ __forceinline__ void dec_tile(const DecItem& it, int j, int& seg, int& nvalid) {
+  if (j < it.tv) { seg = 0; nvalid = min(PAGE, it.vl - j * PAGE); }
+  else if (j < it.tv + it.tt) { seg = 1; nvalid = min(PAGE, it.nt - (j - it.tv) * PAGE); }
+  else { seg = 2; nvalid = min(PAGE, it.na - (j - it.tv - it.tt) * PAGE); }
 }
 
-// tile starting at key k of item `it`: segment, local row, valid keys
-__device__ __forceinline__ void dec_tile(const DecItem& it, int k, int& seg, int& row, int& nvalid) {
-  const int nt = it.nt;
-  int seg_lo, seg_hi;
-  if (k < it.vl) { seg = 0; seg_lo = 0; seg_hi = it.vl; }
-  else if (k < it.vl + nt) { seg = 1; seg_lo = it.vl; seg_hi = it.vl + nt; }
-  else { seg = 2; seg_lo = it.vl + nt; seg_hi = it.hi; }
-  row = k - seg_lo;
-  nvalid = min(TK, min(seg_hi, it.hi) - k);
-}
-
-// FUSED (default): the producer warp classifies each item's Q heads
-// (group_flag_mask, the arithmetic of decode_flags_kernel) and hands the
-// item's active mask to the consumers through a small shared-memory ring —
-// no separate classification launch. (Merging the partials in the CTA that
-// finishes a group's last chunk measured 3.7x slower than the separate merge
-// kernel: the merge lands on few CTAs at the tail.)
+// The producer warp classifies each item's Q heads (group_flag_mask) and
+// hands the item's active mask to the consumers through a small shared-memory
+// ring — no separate classification launch.
 struct FuseArgs {
   const double* k_lazy;
   const double* k_act;
@@ -439,13 +222,9 @@ struct FuseArgs {
 };
 constexpr int NIT = 4;  // item ring depth
 
-template <bool FUSED>
 __global__ void __launch_bounds__((NCW + 1) * 32, 1) decode_partial_tma_kernel(
-    const __grid_constant__ CUtensorMap tm_vk, const __grid_constant__ CUtensorMap tm_vv,
-    const __grid_constant__ CUtensorMap tm_tk, const __grid_constant__ CUtensorMap tm_tv,
-    const __grid_constant__ CUtensorMap tm_ak, const __grid_constant__ CUtensorMap tm_av,
-    const __nv_bfloat16* __restrict__ q, const int32_t* __restrict__ vlen, SegLens sl, int Hq, int Hkv,
-    int vcap, int acap, const uint8_t* __restrict__ flags, float* __restrict__ part_ml,
+    const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
+    const __nv_bfloat16* __restrict__ q, Paged pg, int Hq, int Hkv, float* __restrict__ part_ml,
     float* __restrict__ part_acc, int n_chunks, int total_items, FuseArgs fa, int* __restrict__ degenerate) {
   extern __shared__ uint8_t dsm_raw[];
   __shared__ __align__(8) uint64_t full_bar[NSTG], empty_bar[NSTG];
@@ -475,46 +254,35 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1) decode_partial_tma_kernel(
   if (warp == NCW) {
     // ------------------------------------------------------ TMA producer
     if (lane == 0) {
-      tma_prefetch_desc(&tm_vk); tma_prefetch_desc(&tm_vv);
-      tma_prefetch_desc(&tm_tk); tma_prefetch_desc(&tm_tv);
-      tma_prefetch_desc(&tm_ak); tma_prefetch_desc(&tm_av);
+      tma_prefetch_desc(&tm_k);
+      tma_prefetch_desc(&tm_v);
     }
     uint32_t n = 0, ni = 0;
     for (int t = blockIdx.x; t < total_items; t += gridDim.x, ++ni) {
-      DecItem it;
-      if constexpr (FUSED) {
-        const int s_ = t / (n_chunks * Hkv), g_ = (t / n_chunks) % Hkv;
-        const uint32_t mask = group_flag_mask(q, fa.k_lazy, fa.k_act, s_, g_, Hq, Hkv, fa.tau, fa.preserve,
-                                              fa.flags_override, s_kstage);
-        it = dec_item_mask(t, n_chunks, Hkv, sl, vlen, mask);
-        if (it.c == 0 && lane < rep) fa.flags_out[(size_t)it.s * Hq + it.g * rep + lane] = (mask >> lane) & 1u;
-        const int slot = ni % NIT;
-        if (ni >= NIT) mbar_wait(smem_u32(&item_empty[slot]), ((ni / NIT) - 1) & 1);
-        if (lane == 0) {
-          s_mask[slot] = mask;
-          mbar_arrive(smem_u32(&item_full[slot]));  // release: the mask write precedes it
-        }
-      } else {
-        it = dec_item(t, n_chunks, Hq, Hkv, sl, vlen, flags);
+      const int s_ = t / (n_chunks * Hkv), g_ = (t / n_chunks) % Hkv;
+      const uint32_t mask = group_flag_mask(q, fa.k_lazy, fa.k_act, s_, g_, Hq, Hkv, fa.tau, pg.scale, fa.preserve,
+                                            fa.flags_override, s_kstage);
+      const DecItem it = dec_item(t, n_chunks, Hkv, pg, mask);
+      if (it.c == 0 && lane < rep) fa.flags_out[(size_t)it.s * Hq + it.g * rep + lane] = (mask >> lane) & 1u;
+      const int slot = ni % NIT;
+      if (ni >= NIT) mbar_wait(smem_u32(&item_empty[slot]), ((ni / NIT) - 1) & 1);
+      if (lane == 0) {
+        s_mask[slot] = mask;
+        mbar_arrive(smem_u32(&item_full[slot]));  // release: the mask write precedes it
       }
       if (lane == 0) {
-        const int sg = it.s * Hkv + it.g;
-        for (int k = it.lo; k < it.hi; k += TK) {
-          int seg, row, nv;
-          dec_tile(it, k, seg, row, nv);
-          k += nv - TK;  // next tile starts after this tile's valid keys (segment-aligned)
+        const int32_t* pages = pg.table + (size_t)(it.s * Hkv + it.g) * pg.max_pages;
+        for (int j = it.t0; j < it.t1; ++j) {
+          const int row = __ldg(pages + j) * PAGE;
           const int st = n % NSTG;
           if (n >= NSTG) mbar_wait(smem_u32(&empty_bar[st]), ((n / NSTG) - 1) & 1);
           const uint32_t fb = smem_u32(&full_bar[st]);
           mbar_expect_tx(fb, TSTAGE);
-          const CUtensorMap* mk = seg == 0 ? &tm_vk : seg == 1 ? &tm_tk : &tm_ak;
-          const CUtensorMap* mv = seg == 0 ? &tm_vv : seg == 1 ? &tm_tv : &tm_av;
-          const int base = seg == 0 ? sg * vcap : seg == 1 ? sg * sl.tcap : sg * acap;
           const uint32_t kd = sbase + st * TSTAGE, vd = kd + TTILE;
-          tma_load_2d(kd, mk, fb, 0, base + row);
-          tma_load_2d(kd + TATOM, mk, fb, 64, base + row);
-          tma_load_2d(vd, mv, fb, 0, base + row);
-          tma_load_2d(vd + TATOM, mv, fb, 64, base + row);
+          tma_load_2d(kd, &tm_k, fb, 0, row);
+          tma_load_2d(kd + TATOM, &tm_k, fb, 64, row);
+          tma_load_2d(vd, &tm_v, fb, 0, row);
+          tma_load_2d(vd + TATOM, &tm_v, fb, 64, row);
           ++n;
         }
       }
@@ -525,23 +293,16 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1) decode_partial_tma_kernel(
   // ------------------------------------------------------ consumers
   const int r4 = lane & 3, gid = lane >> 2;
   const bool row_valid = gid < rep;
-  const float sl2 = static_cast<float>(kLog2e / sqrt(static_cast<double>(D)));
+  const float sl2 = static_cast<float>(kLog2e * pg.scale);
   uint32_t n = 0, ni = 0;
   for (int t = blockIdx.x; t < total_items; t += gridDim.x, ++ni) {
-    DecItem it;
-    bool row_vis;
-    if constexpr (FUSED) {
-      const int slot = ni % NIT;
-      mbar_wait(smem_u32(&item_full[slot]), (ni / NIT) & 1);
-      const uint32_t mask = s_mask[slot];
-      __syncwarp();
-      if (lane == 0) mbar_arrive(smem_u32(&item_empty[slot]));
-      it = dec_item_mask(t, n_chunks, Hkv, sl, vlen, mask);
-      row_vis = row_valid && ((mask >> gid) & 1u);
-    } else {
-      it = dec_item(t, n_chunks, Hq, Hkv, sl, vlen, flags);
-      row_vis = row_valid && flags[(size_t)it.s * Hq + it.g * rep + (row_valid ? gid : 0)];
-    }
+    const int slot = ni % NIT;
+    mbar_wait(smem_u32(&item_full[slot]), (ni / NIT) & 1);
+    const uint32_t mask = s_mask[slot];
+    __syncwarp();
+    if (lane == 0) mbar_arrive(smem_u32(&item_empty[slot]));
+    const DecItem it = dec_item(t, n_chunks, Hkv, pg, mask);
+    const bool row_vis = row_valid && ((mask >> gid) & 1u);
     // Q A-fragments, natural head-dim order: k-step ks covers d = 16 ks .. +15
     uint32_t qa[8][4];
     {
@@ -559,15 +320,13 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1) decode_partial_tma_kernel(
     float acc[16][4];
 #pragma unroll
     for (int i = 0; i < 16; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
-    for (int k = it.lo; k < it.hi; k += TK) {
-      int seg, row, nv;
-      dec_tile(it, k, seg, row, nv);
-      const int key0 = k;
-      k += nv - TK;
+    for (int j = it.t0; j < it.t1; ++j) {
+      int seg, nv;
+      dec_tile(it, j, seg, nv);
       const int st = n % NSTG;
       mbar_wait(smem_u32(&full_bar[st]), (n / NSTG) & 1);
       const uint32_t kt = sbase + st * TSTAGE, vt = kt + TTILE;
-      const int w0 = warp * 16;  // this warp's first key of the tile
+      const int w0 = warp * 16;  // this warp's first key of the page
       if (w0 < nv) {
         // ---- S = Q K^T over 16 keys (two n-tiles of 8)
         float sc[2][4];
@@ -582,13 +341,13 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1) decode_partial_tma_kernel(
           mma_bf16_16816(sc[0], qa[ks], b[0], b[1]);
           mma_bf16_16816(sc[1], qa[ks], b[2], b[3]);
         }
-        // ---- mask (keys beyond the tile; vision keys for lazy heads), online softmax
+        // ---- mask (rows past the page's valid rows; vision keys for lazy heads), online softmax
         float x[4];
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
-            const int kk = w0 + 8 * u + 2 * r4 + e;  // key within the tile
+            const int kk = w0 + 8 * u + 2 * r4 + e;  // key within the page
             const bool ok = row_valid && kk < nv && (seg != 0 || row_vis);
             x[2 * u + e] = ok ? sc[u][e] * sl2 : -INFINITY;
           }
@@ -617,12 +376,12 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1) decode_partial_tma_kernel(
         uint32_t pa[4] = {pack_bf16x2(p[0], p[1]), 0u, pack_bf16x2(p[2], p[3]), 0u};
         // ---- O += P V over 16 d n-tiles (pairs from one ldmatrix.x4.trans)
 #pragma unroll
-        for (int j = 0; j < 16; j += 2) {
+        for (int jj = 0; jj < 16; jj += 2) {
           uint32_t b[4];
-          // matrices: (keys 0-7, d 8j) (keys 8-15, d 8j) (keys 0-7, d 8j+8) (keys 8-15, d 8j+8)
-          ldsm_x4_t(vt + toff(w0 + (mi & 1) * 8 + rr, j + (mi >> 1)), b);
-          mma_bf16_16816(acc[j], pa, b[0], b[1]);
-          mma_bf16_16816(acc[j + 1], pa, b[2], b[3]);
+          // matrices: (keys 0-7, d 8jj) (keys 8-15, d 8jj) (keys 0-7, d 8jj+8) (keys 8-15, d 8jj+8)
+          ldsm_x4_t(vt + toff(w0 + (mi & 1) * 8 + rr, jj + (mi >> 1)), b);
+          mma_bf16_16816(acc[jj], pa, b[0], b[1]);
+          mma_bf16_16816(acc[jj + 1], pa, b[2], b[3]);
         }
       }
       __syncwarp();
@@ -637,11 +396,11 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1) decode_partial_tma_kernel(
         s_ml[warp][gid][0] = m_run;
         s_ml[warp][gid][1] = l_run;
       }
-      // C fragment of n-tile j: acc[j][0/1] = O[row gid][d = 8 j + 2 r4 + {0,1}]
+      // C fragment of n-tile jj: acc[jj][0/1] = O[row gid][d = 8 jj + 2 r4 + {0,1}]
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        s_acc[warp][gid][8 * j + 2 * r4] = acc[j][0];
-        s_acc[warp][gid][8 * j + 2 * r4 + 1] = acc[j][1];
+      for (int jj = 0; jj < 16; ++jj) {
+        s_acc[warp][gid][8 * jj + 2 * r4] = acc[jj][0];
+        s_acc[warp][gid][8 * jj + 2 * r4 + 1] = acc[jj][1];
       }
     }
     named_bar_sync(1, NCW * 32);
@@ -650,23 +409,68 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1) decode_partial_tma_kernel(
       float M = -INFINITY;
 #pragma unroll
       for (int w = 0; w < NCW; ++w) M = fmaxf(M, s_ml[w][r][0]);
-      float L = 0.f, o = 0.f;
+      float Lsum = 0.f, o = 0.f;
 #pragma unroll
       for (int w = 0; w < NCW; ++w) {
         const float m = s_ml[w][r][0];
         if (m == -INFINITY) continue;
         const float wt = fast_exp2(m - M);
-        L += wt * s_ml[w][r][1];
+        Lsum += wt * s_ml[w][r][1];
         o += wt * s_acc[w][r][col];
       }
       const size_t pb = ((size_t)it.s * Hq + it.g * rep + r) * n_chunks + it.c;
       part_acc[pb * D + col] = o;
       if (col == 0) {
         part_ml[pb * 2 + 0] = M;
-        part_ml[pb * 2 + 1] = L;
+        part_ml[pb * 2 + 1] = Lsum;
       }
     }
     named_bar_sync(1, NCW * 32);  // partial slots free for the next item
+  }
+}
+
+// append_answer (decode.py:111-121) for a batch, one launch: the new K / V
+// row of every (sequence, KV group) goes to answer row a = alen[s] — page slot
+// pages(vlen) + pages(tlen) + a / 64 of the group's list (allocated by the
+// host beforehand), row a % 64 — and alen[s] advances. One CTA per sequence,
+// so the position is read before it is advanced.
+__global__ void append_paged_kernel(const uint4* __restrict__ k_rows, const uint4* __restrict__ v_rows,
+                                    uint4* __restrict__ pool_k, uint4* __restrict__ pool_v, Paged pg, int Hkv,
+                                    int32_t* __restrict__ alen) {
+  constexpr int RV = D * 2 / 16;  // uint4 per bf16 row
+  const int s = blockIdx.x;
+  const int a = alen[s];
+  const int slot = pages_of(pg.vlen[s]) + pages_of(pg.tlen[s]) + a / PAGE;
+  for (int e = threadIdx.x; e < Hkv * RV; e += blockDim.x) {
+    const int g = e / RV, c = e % RV;
+    const int page = pg.table[((size_t)s * Hkv + g) * pg.max_pages + slot];
+    const size_t src = ((size_t)s * Hkv + g) * RV + c;
+    const size_t dst = ((size_t)page * PAGE + a % PAGE) * RV + c;
+    pool_k[dst] = k_rows[src];
+    pool_v[dst] = v_rows[src];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) alen[s] = a + 1;
+}
+
+// Rows into pages (K6 for the paged cache): for group g and r < count,
+// pool[page(g, first_slot + (row0 + r) / 64) * 64 + (row0 + r) % 64] =
+// src[g, idx ? idx[g, r] : r]; the rest of the last page is zero-filled.
+__global__ void page_write_kernel(const uint4* __restrict__ src, int src_rows, const int32_t* __restrict__ idx,
+                                  int idx_stride, int count, const int32_t* __restrict__ table, int max_pages,
+                                  int first_slot, uint4* __restrict__ pool) {
+  constexpr int RV = D * 2 / 16;
+  const int g = blockIdx.y;
+  const int r = blockIdx.x * (blockDim.x / RV) + threadIdx.x / RV, c = threadIdx.x % RV;
+  const int padded = pages_of(count) * PAGE;
+  if (r >= padded) return;
+  const int page = table[(size_t)g * max_pages + first_slot + r / PAGE];
+  const size_t dst = ((size_t)page * PAGE + r % PAGE) * RV + c;
+  if (r < count) {
+    const int sr = idx ? idx[(size_t)g * idx_stride + r] : r;
+    pool[dst] = src[((size_t)g * src_rows + sr) * RV + c];
+  } else {
+    pool[dst] = make_uint4(0, 0, 0, 0);
   }
 }
 
@@ -678,166 +482,75 @@ using namespace omni;
 int omni_make_tmap_rows(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols_elems, int elem_bytes,
                         uint32_t box_cols, uint32_t box_rows);
 
-static int dec_chunks(int vcap, int n_text, int n_answer) {
-  return (vcap + n_text + n_answer + dec::CTA_KEYS - 1) / dec::CTA_KEYS;
+extern "C" size_t omni_decode_workspace(int batch, int n_q_heads, int n_chunks) {
+  return sizeof(float) * (size_t)batch * n_q_heads * n_chunks * (dec::D + 2) + 16;
 }
 
-extern "C" size_t omni_decode_workspace(int batch, int n_q_heads, int vcap, int n_text, int acap, int head_dim) {
-  const int nc = dec_chunks(vcap, n_text, acap);
-  return sizeof(float) * (size_t)batch * n_q_heads * nc * (head_dim + 2) + 16;
-}
-
-static int decode_step_impl(const void* q, const void* vision_k, const void* vision_v, const int32_t* vision_len,
-                            const void* text_k, const void* text_v, const void* answer_k, const void* answer_v,
-                            dec::SegLens sl, const double* k_lazy, const double* k_act, int batch, int n_q_heads,
-                            int n_kv_heads, int head_dim, int vcap, int acap, double tau, int preserve_first_head,
-                            const uint8_t* flags_override, uint8_t* flags, float* out, void* workspace,
-                            int32_t* status, void* stream) {
-  OMNI_CHECK(head_dim == dec::D, OMNI_E_SHAPE, "decode kernel requires head_dim == 128");
+extern "C" int omni_decode(const void* q, const void* pool_k, const void* pool_v, int n_pages, const int32_t* table,
+                           int max_pages, const int32_t* vision_len, const int32_t* text_len,
+                           const int32_t* answer_len, int n_chunks, const double* k_lazy, const double* k_act,
+                           int batch, int n_q_heads, int n_kv_heads, int head_dim, double tau,
+                           int preserve_first_head, const uint8_t* flags_override, uint8_t* flags, float* out,
+                           void* workspace, int32_t* status, void* stream) {
+  omni_begin();
+  OMNI_CHECK(head_dim >= 1 && head_dim <= dec::D, OMNI_E_SHAPE,
+             "decode rows are stored with 128 columns: head_dim must be in [1, 128] (zero-pad shorter rows)");
   OMNI_CHECK(n_kv_heads >= 1 && n_q_heads % n_kv_heads == 0, OMNI_E_SHAPE, "n_q_heads must be a multiple of n_kv_heads");
   OMNI_CHECK(n_q_heads / n_kv_heads <= dec::MAXREP, OMNI_E_SHAPE, "at most 8 Q heads per KV group");
   OMNI_CHECK(tau >= 0.0 && tau < 1.0, OMNI_E_PARAM, "tau must be in [0, 1)");
-  OMNI_CHECK(batch >= 1, OMNI_E_SHAPE, "empty batch");
-  const int n_text = sl.tcap;
-  const int n_answer = sl.alen ? acap : sl.na;
+  OMNI_CHECK(batch >= 1 && n_pages >= 1 && max_pages >= 1 && n_chunks >= 1, OMNI_E_SHAPE, "empty batch or pool");
+  OMNI_CHECK(vision_len && text_len && answer_len && status && table, OMNI_E_PARAM,
+             "decode needs the page table, the three length vectors and a status word");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const int nc = dec_chunks(vcap, n_text, n_answer);
   float* part_ml = static_cast<float*>(workspace);
-  float* part_acc = part_ml + (size_t)batch * n_q_heads * nc * 2;
-  int* degenerate = status ? reinterpret_cast<int*>(status)
-                           : reinterpret_cast<int*>(part_acc + (size_t)batch * n_q_heads * nc * head_dim);
-  // K7 implementation: the TMA-staged persistent kernel with the query
-  // classification fused in by default, then the split-K merge;
-  // OMNI_DECODE_IMPL=split classifies in a separate kernel first,
-  // OMNI_DECODE_IMPL=regs uses the register-staged partial kernel.
-  static const int impl = [] {
-    const char* e = getenv("OMNI_DECODE_IMPL");
-    return (e && strcmp(e, "regs") == 0) ? 2 : (e && strcmp(e, "split") == 0) ? 1 : 0;
-  }();
-  const bool regs = impl == 2, fused = impl == 0;
-  if (!fused)
-    dec::decode_flags_kernel<<<dim3(n_kv_heads, batch), 32, 0, st>>>(static_cast<const __nv_bfloat16*>(q), k_lazy,
-                                                                      k_act, n_q_heads, n_kv_heads, tau,
-                                                                      preserve_first_head, flags_override, flags);
-  if (regs) {
-    dec::decode_partial_kernel<<<dim3(nc, n_kv_heads, batch), 128, 0, st>>>(
-        static_cast<const __nv_bfloat16*>(q), static_cast<const __nv_bfloat16*>(vision_k),
-        static_cast<const __nv_bfloat16*>(vision_v), vision_len, static_cast<const __nv_bfloat16*>(text_k),
-        static_cast<const __nv_bfloat16*>(text_v), static_cast<const __nv_bfloat16*>(answer_k),
-        static_cast<const __nv_bfloat16*>(answer_v), sl, n_q_heads, n_kv_heads, vcap, acap, flags, part_ml,
-        part_acc, nc, degenerate);
-  } else {
-    CUtensorMap m[6];
-    const uint64_t vrows = (uint64_t)batch * n_kv_heads * vcap;
-    const void* bases[6] = {vision_k, vision_v, n_text > 0 ? text_k : vision_k, n_text > 0 ? text_v : vision_v,
-                            acap > 0 ? answer_k : vision_k, acap > 0 ? answer_v : vision_v};
-    const uint64_t rows[6] = {vrows, vrows, n_text > 0 ? (uint64_t)batch * n_kv_heads * n_text : vrows,
-                              n_text > 0 ? (uint64_t)batch * n_kv_heads * n_text : vrows,
-                              acap > 0 ? (uint64_t)batch * n_kv_heads * acap : vrows,
-                              acap > 0 ? (uint64_t)batch * n_kv_heads * acap : vrows};
-    for (int i = 0; i < 6; ++i) {
-      const int rc = omni_make_tmap_rows(&m[i], bases[i], rows[i], dec::D, 2, 64, dec::TK);
-      if (rc) return rc;
-    }
-    auto kern = fused ? dec::decode_partial_tma_kernel<true> : dec::decode_partial_tma_kernel<false>;
-    static bool attr[2] = {false, false};
-    if (!attr[fused]) {
-      OMNI_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dec::TSMEM));
-      attr[fused] = true;
-    }
-    int dev = 0, sms = 148;
-    OMNI_CUDA_TRY(cudaGetDevice(&dev));
-    OMNI_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    const int items = nc * n_kv_heads * batch;
-    const dec::FuseArgs fa{k_lazy, k_act, tau, preserve_first_head, flags_override, flags};
-    kern<<<min(sms, items), (dec::NCW + 1) * 32, dec::TSMEM, st>>>(
-        m[0], m[1], m[2], m[3], m[4], m[5], static_cast<const __nv_bfloat16*>(q), vision_len, sl, n_q_heads,
-        n_kv_heads, vcap, acap, flags, part_ml, part_acc, nc, items, fa, degenerate);
-  }
-  dec::decode_combine_kernel<<<dim3(n_q_heads, batch), dec::D, 0, st>>>(part_ml, part_acc, nc, out, degenerate);
-  int st_code = omni_launch_check();
-  if (st_code) return st_code;
-  if (!status && n_text + n_answer == 0) {
-    // Only reachable degenerate case (decode.py:152-153): read the flag back.
-    int h = 0;
-    OMNI_CUDA_TRY(cudaMemcpyAsync(&h, degenerate, sizeof(int), cudaMemcpyDeviceToHost, st));
-    OMNI_CUDA_TRY(cudaStreamSynchronize(st));
-    OMNI_CHECK(h == 0, OMNI_E_DEGENERATE_CONTEXT, "lazy head with no text and no answer KV");
-  }
-  return OMNI_OK;
+  float* part_acc = part_ml + (size_t)batch * n_q_heads * n_chunks * 2;
+  CUtensorMap mk, mv;
+  int rc = omni_make_tmap_rows(&mk, pool_k, (uint64_t)n_pages * dec::PAGE, dec::D, 2, 64, dec::PAGE);
+  if (rc) return rc;
+  rc = omni_make_tmap_rows(&mv, pool_v, (uint64_t)n_pages * dec::PAGE, dec::D, 2, 64, dec::PAGE);
+  if (rc) return rc;
+  OMNI_CUDA_TRY(omni_smem_attr(dec::decode_partial_tma_kernel, (int)dec::TSMEM));
+  int dev = 0, sms = 148;
+  OMNI_CUDA_TRY(cudaGetDevice(&dev));
+  OMNI_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const int items = n_chunks * n_kv_heads * batch;
+  const dec::Paged pg{table, max_pages, vision_len, text_len, answer_len, 1.0 / sqrt(static_cast<double>(head_dim))};
+  const dec::FuseArgs fa{k_lazy, k_act, tau, preserve_first_head, flags_override, flags};
+  dec::decode_partial_tma_kernel<<<min(sms, items), (dec::NCW + 1) * 32, dec::TSMEM, st>>>(
+      mk, mv, static_cast<const __nv_bfloat16*>(q), pg, n_q_heads, n_kv_heads, part_ml, part_acc, n_chunks, items,
+      fa, status);
+  dec::decode_combine_kernel<<<dim3(n_q_heads, batch), dec::D, 0, st>>>(part_ml, part_acc, n_chunks, out, status);
+  return omni_launch_check();
 }
 
-extern "C" int omni_decode_step(const void* q, const void* vision_k, const void* vision_v, const int32_t* vision_len,
-                                const void* text_k, const void* text_v, int n_text, const void* answer_k,
-                                const void* answer_v, int n_answer, const double* k_lazy, const double* k_act,
-                                int batch, int n_q_heads, int n_kv_heads, int head_dim, int vcap, int acap, double tau,
-                                int preserve_first_head, const uint8_t* flags_override, uint8_t* flags, float* out,
-                                void* workspace, void* stream) {
-  OMNI_CHECK(n_answer >= 0 && n_answer <= acap && n_text >= 0, OMNI_E_SHAPE, "answer segment overflow");
-  const dec::SegLens sl{nullptr, nullptr, n_text, n_answer, n_text};
-  return decode_step_impl(q, vision_k, vision_v, vision_len, text_k, text_v, answer_k, answer_v, sl, k_lazy, k_act,
-                          batch, n_q_heads, n_kv_heads, head_dim, vcap, acap, tau, preserve_first_head,
-                          flags_override, flags, out, workspace, nullptr, stream);
-}
-
-extern "C" int omni_decode_step_varlen(const void* q, const void* vision_k, const void* vision_v,
-                                       const int32_t* vision_len, const void* text_k, const void* text_v,
-                                       const int32_t* text_len, int tcap, const void* answer_k, const void* answer_v,
-                                       const int32_t* answer_len, const double* k_lazy, const double* k_act,
-                                       int batch, int n_q_heads, int n_kv_heads, int head_dim, int vcap, int acap,
-                                       double tau, int preserve_first_head, const uint8_t* flags_override,
-                                       uint8_t* flags, float* out, void* workspace, int32_t* status, void* stream) {
-  OMNI_CHECK(text_len && answer_len && status, OMNI_E_PARAM, "varlen decode needs text_len, answer_len and status");
-  OMNI_CHECK(tcap >= 0 && acap >= 0 && tcap + acap > 0, OMNI_E_SHAPE, "text and answer capacities are both zero");
-  const dec::SegLens sl{text_len, answer_len, 0, 0, tcap};
-  return decode_step_impl(q, vision_k, vision_v, vision_len, text_k, text_v, answer_k, answer_v, sl, k_lazy, k_act,
-                          batch, n_q_heads, n_kv_heads, head_dim, vcap, acap, tau, preserve_first_head,
-                          flags_override, flags, out, workspace, status, stream);
-}
-
-// SURVEY §8b's minimum export set names the decode entry point omni_decode;
-// it is omni_decode_step.
-extern "C" int omni_decode(const void* q, const void* vision_k, const void* vision_v, const int32_t* vision_len,
-                           const void* text_k, const void* text_v, int n_text, const void* answer_k,
-                           const void* answer_v, int n_answer, const double* k_lazy, const double* k_act, int batch,
-                           int n_q_heads, int n_kv_heads, int head_dim, int vcap, int acap, double tau,
-                           int preserve_first_head, const uint8_t* flags_override, uint8_t* flags, float* out,
-                           void* workspace, void* stream) {
-  return omni_decode_step(q, vision_k, vision_v, vision_len, text_k, text_v, n_text, answer_k, answer_v, n_answer,
-                          k_lazy, k_act, batch, n_q_heads, n_kv_heads, head_dim, vcap, acap, tau, preserve_first_head,
-                          flags_override, flags, out, workspace, stream);
-}
-
-// append_answer (decode.py:111-121) for a batch, one launch: the new K / V row
-// of every (sequence, KV group) goes to answer row pos_s = answer_len[s]
-// (ragged batches; incremented here) or n_answer (answer_len NULL). One CTA
-// per sequence, so the position is read before it is advanced.
-__global__ void append_answer_kernel(const uint4* __restrict__ k_rows, const uint4* __restrict__ v_rows,
-                                     uint4* __restrict__ ak, uint4* __restrict__ av, int Hkv, int acap, int n_answer,
-                                     int32_t* __restrict__ answer_len) {
-  constexpr int RV = dec::D * 2 / 16;  // uint4 per bf16 row
-  const int s = blockIdx.x;
-  const int pos = answer_len ? answer_len[s] : n_answer;
-  for (int e = threadIdx.x; e < Hkv * RV; e += blockDim.x) {
-    const int g = e / RV, c = e % RV;
-    const size_t src = ((size_t)s * Hkv + g) * RV + c;
-    const size_t dst = (((size_t)s * Hkv + g) * acap + pos) * RV + c;
-    ak[dst] = k_rows[src];
-    av[dst] = v_rows[src];
-  }
-  __syncthreads();
-  if (answer_len && threadIdx.x == 0) answer_len[s] = pos + 1;
-}
-
-extern "C" int omni_append_answer(const void* k_rows, const void* v_rows, void* answer_k, void* answer_v, int batch,
-                                  int n_kv_heads, int head_dim, int acap, int n_answer, int32_t* answer_len,
-                                  void* stream) {
-  OMNI_CHECK(head_dim == dec::D, OMNI_E_SHAPE, "answer rows must have head_dim 128");
-  OMNI_CHECK(answer_len != nullptr || (n_answer >= 0 && n_answer < acap), OMNI_E_SHAPE, "answer capacity exhausted");
+extern "C" int omni_append_answer(const void* k_rows, const void* v_rows, void* pool_k, void* pool_v,
+                                  const int32_t* table, int max_pages, const int32_t* vision_len,
+                                  const int32_t* text_len, int32_t* answer_len, int batch, int n_kv_heads,
+                                  int head_dim, void* stream) {
+  omni_begin();
+  OMNI_CHECK(head_dim >= 1 && head_dim <= dec::D, OMNI_E_SHAPE, "answer rows are stored with 128 columns");
+  OMNI_CHECK(table && vision_len && text_len && answer_len, OMNI_E_PARAM, "append needs the page table and lengths");
   if (batch == 0) return OMNI_OK;
-  append_answer_kernel<<<batch, 128, 0, static_cast<cudaStream_t>(stream)>>>(
-      static_cast<const uint4*>(k_rows), static_cast<const uint4*>(v_rows), static_cast<uint4*>(answer_k),
-      static_cast<uint4*>(answer_v), n_kv_heads, acap, n_answer, answer_len);
+  const dec::Paged pg{table, max_pages, vision_len, text_len, answer_len, 0.0};
+  dec::append_paged_kernel<<<batch, 128, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const uint4*>(k_rows), static_cast<const uint4*>(v_rows), static_cast<uint4*>(pool_k),
+      static_cast<uint4*>(pool_v), pg, n_kv_heads, answer_len);
+  return omni_launch_check();
+}
+
+extern "C" int omni_page_write(const void* src, int n_groups, int src_rows, int head_dim, const int32_t* idx,
+                               int idx_stride, int count, const int32_t* table, int max_pages, int first_slot,
+                               void* pool, void* stream) {
+  omni_begin();
+  OMNI_CHECK(head_dim == dec::D, OMNI_E_SHAPE, "page rows are 128 bf16 columns (zero-pad shorter rows first)");
+  OMNI_CHECK(count >= 0 && n_groups >= 0 && first_slot >= 0, OMNI_E_SHAPE, "negative extent");
+  if (count == 0 || n_groups == 0) return OMNI_OK;
+  const int rows_per_cta = 256 / (dec::D * 2 / 16);  // 16
+  const int padded = (count + dec::PAGE - 1) / dec::PAGE * dec::PAGE;
+  dec::page_write_kernel<<<dim3((padded + rows_per_cta - 1) / rows_per_cta, n_groups), 256, 0,
+                           static_cast<cudaStream_t>(stream)>>>(static_cast<const uint4*>(src), src_rows, idx,
+                                                                idx_stride, count, table, max_pages, first_slot,
+                                                                static_cast<uint4*>(pool));
   return omni_launch_check();
 }
 
@@ -846,13 +559,59 @@ extern "C" int omni_append_answer(const void* k_rows, const void* v_rows, void* 
 extern "C" int omni_decode_flags(const void* q, const double* k_lazy, const double* k_act, int batch, int n_q_heads,
                                  int n_kv_heads, int head_dim, double tau, int preserve_first_head, uint8_t* flags,
                                  void* stream) {
-  OMNI_CHECK(head_dim == dec::D, OMNI_E_SHAPE, "decode classification requires head_dim == 128");
+  omni_begin();
+  OMNI_CHECK(head_dim >= 1 && head_dim <= dec::D, OMNI_E_SHAPE, "decode queries are stored with 128 columns");
   OMNI_CHECK(n_kv_heads >= 1 && n_q_heads % n_kv_heads == 0 && n_q_heads / n_kv_heads <= dec::MAXREP, OMNI_E_SHAPE,
              "need Hq a multiple of Hkv with at most 8 Q heads per group");
   OMNI_CHECK(tau >= 0.0 && tau < 1.0, OMNI_E_PARAM, "tau must be in [0, 1)");
   if (batch == 0) return OMNI_OK;
   dec::decode_flags_kernel<<<dim3(n_kv_heads, batch), 32, 0, static_cast<cudaStream_t>(stream)>>>(
-      static_cast<const __nv_bfloat16*>(q), k_lazy, k_act, n_q_heads, n_kv_heads, tau, preserve_first_head, nullptr,
-      flags);
+      static_cast<const __nv_bfloat16*>(q), k_lazy, k_act, n_q_heads, n_kv_heads, tau,
+      1.0 / sqrt(static_cast<double>(head_dim)), preserve_first_head, nullptr, flags);
+  return omni_launch_check();
+}
+
+namespace omni {
+namespace dec {
+// classify_decode_query (decode.py:124-140) on float64 queries (the
+// reference's own precision, for the reference-signature operators): one warp
+// per (sequence, Q head), logits q . k / sqrt(head_dim) over the logical head
+// dims, the max-subtracted two-way softmax and the strict p_act > tau.
+__global__ void decode_flags_f64_kernel(const double* __restrict__ q, const double* __restrict__ k_lazy,
+                                        const double* __restrict__ k_act, int Hq, int Hkv, int dl, int ldk,
+                                        double tau, int preserve, uint8_t* __restrict__ flags) {
+  const int h = blockIdx.x, s = blockIdx.y, lane = threadIdx.x, g = h / (Hq / Hkv);
+  const double* qr = q + ((size_t)s * Hq + h) * dl;
+  const double* kl = k_lazy + ((size_t)s * Hkv + g) * ldk;
+  const double* ka = k_act + ((size_t)s * Hkv + g) * ldk;
+  double a = 0.0, b = 0.0;
+  for (int c = lane; c < dl; c += 32) {
+    a = fma(qr[c], kl[c], a);
+    b = fma(qr[c], ka[c], b);
+  }
+  a = warp_sum(a);
+  b = warp_sum(b);
+  if (lane == 0) {
+    const double scale = 1.0 / sqrt(static_cast<double>(dl));
+    const double l0 = a * scale, l1 = b * scale, mx = fmax(l0, l1);
+    const double e0 = exp(l0 - mx), e1 = exp(l1 - mx);
+    int f = (e1 / (e0 + e1) > tau) ? 1 : 0;
+    if (preserve && h == 0) f = 1;
+    flags[(size_t)s * Hq + h] = static_cast<uint8_t>(f);
+  }
+}
+}  // namespace dec
+}  // namespace omni
+
+extern "C" int omni_decode_flags_f64(const double* q, const double* k_lazy, const double* k_act, int batch,
+                                     int n_q_heads, int n_kv_heads, int head_dim, int probe_stride, double tau,
+                                     int preserve_first_head, uint8_t* flags, void* stream) {
+  omni_begin();
+  OMNI_CHECK(head_dim >= 1 && head_dim <= probe_stride, OMNI_E_SHAPE, "head_dim exceeds the probe-key row stride");
+  OMNI_CHECK(n_kv_heads >= 1 && n_q_heads % n_kv_heads == 0, OMNI_E_SHAPE, "n_q_heads must be a multiple of n_kv_heads");
+  OMNI_CHECK(tau >= 0.0 && tau < 1.0, OMNI_E_PARAM, "tau must be in [0, 1)");
+  if (batch == 0) return OMNI_OK;
+  dec::decode_flags_f64_kernel<<<dim3(n_q_heads, batch), 32, 0, static_cast<cudaStream_t>(stream)>>>(
+      q, k_lazy, k_act, n_q_heads, n_kv_heads, head_dim, probe_stride, tau, preserve_first_head, flags);
   return omni_launch_check();
 }

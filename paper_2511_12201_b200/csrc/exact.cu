@@ -129,6 +129,7 @@ extern "C" size_t omni_exact_mass_workspace(int n_q_heads, int seq_len) {
 
 extern "C" int omni_exact_mass(const void* Q, const void* K, int dtype, int n_q_heads, int n_kv_heads, int seq_len,
                                int head_dim, double* mass, void* workspace, void* stream) {
+  omni_begin();
   OMNI_CHECK(n_kv_heads >= 1 && n_q_heads % n_kv_heads == 0, OMNI_E_SHAPE, "n_q_heads must be a multiple of n_kv_heads");
   OMNI_CHECK(head_dim >= 1 && head_dim <= 256, OMNI_E_SHAPE, "head_dim must be in [1, 256]");
   OMNI_CHECK(seq_len >= 1, OMNI_E_SHAPE, "empty sequence");
@@ -140,15 +141,22 @@ extern "C" int omni_exact_mass(const void* Q, const void* K, int dtype, int n_q_
   if (dtype == OMNI_DTYPE_BF16) {
     auto q = static_cast<const __nv_bfloat16*>(Q);
     auto k = static_cast<const __nv_bfloat16*>(K);
-    OMNI_CUDA_TRY(cudaFuncSetAttribute(exact::row_pass_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
-    OMNI_CUDA_TRY(cudaFuncSetAttribute(exact::col_pass_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
+    OMNI_CUDA_TRY(omni_smem_attr(exact::row_pass_kernel<__nv_bfloat16>, (int)shm));
+    OMNI_CUDA_TRY(omni_smem_attr(exact::col_pass_kernel<__nv_bfloat16>, (int)shm));
     exact::row_pass_kernel<<<grid, 256, shm, s>>>(q, k, seq_len, head_dim, rep, stats);
     exact::col_pass_kernel<<<grid, 256, shm, s>>>(q, k, seq_len, head_dim, rep, stats, mass);
   } else if (dtype == OMNI_DTYPE_F32) {
     auto q = static_cast<const float*>(Q);
     auto k = static_cast<const float*>(K);
-    OMNI_CUDA_TRY(cudaFuncSetAttribute(exact::row_pass_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
-    OMNI_CUDA_TRY(cudaFuncSetAttribute(exact::col_pass_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
+    OMNI_CUDA_TRY(omni_smem_attr(exact::row_pass_kernel<float>, (int)shm));
+    OMNI_CUDA_TRY(omni_smem_attr(exact::col_pass_kernel<float>, (int)shm));
+    exact::row_pass_kernel<<<grid, 256, shm, s>>>(q, k, seq_len, head_dim, rep, stats);
+    exact::col_pass_kernel<<<grid, 256, shm, s>>>(q, k, seq_len, head_dim, rep, stats, mass);
+  } else if (dtype == OMNI_DTYPE_F64) {
+    auto q = static_cast<const double*>(Q);
+    auto k = static_cast<const double*>(K);
+    OMNI_CUDA_TRY(omni_smem_attr(exact::row_pass_kernel<double>, (int)shm));
+    OMNI_CUDA_TRY(omni_smem_attr(exact::col_pass_kernel<double>, (int)shm));
     exact::row_pass_kernel<<<grid, 256, shm, s>>>(q, k, seq_len, head_dim, rep, stats);
     exact::col_pass_kernel<<<grid, 256, shm, s>>>(q, k, seq_len, head_dim, rep, stats, mass);
   } else {

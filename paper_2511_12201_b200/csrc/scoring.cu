@@ -31,6 +31,18 @@ struct Vec8<float> {
   }
 };
 
+template <>
+struct Vec8<double> {
+  __device__ static void load(const double* p, double* out) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const double2 v = __ldg(reinterpret_cast<const double2*>(p) + i);
+      out[2 * i] = v.x;
+      out[2 * i + 1] = v.y;
+    }
+  }
+};
+
 // Raw 8-element vector kept in registers until converted (keeps many rows in
 // flight per thread without paying 16 f64 registers per row).
 template <typename T>
@@ -55,6 +67,20 @@ struct Raw8<float> {
   __device__ double at(int i) const {
     return static_cast<double>(i < 4 ? reinterpret_cast<const float*>(&a)[i] : reinterpret_cast<const float*>(&b)[i - 4]);
   }
+};
+
+template <>
+struct Raw8<double> {  // the reference's own precision (drop-in float64 workloads)
+  double2 v[4];
+  __device__ void load(const double* p) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) v[i] = __ldg(reinterpret_cast<const double2*>(p) + i);
+  }
+  __device__ void zero() {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) v[i] = make_double2(0.0, 0.0);
+  }
+  __device__ double at(int i) const { return (i & 1) ? v[i >> 1].y : v[i >> 1].x; }
 };
 
 // ------------------------------------------------------------------------ K1
@@ -531,6 +557,7 @@ extern "C" size_t omni_kv_probe_workspace(int n_kv_heads, int seq_len, int head_
 extern "C" int omni_kv_probe(const void* K, int dtype, int n_kv_heads, int seq_len, int head_dim, int n_vision,
                              int sink_index, int block_size, double* k_lazy, double* k_act, double* pooled_k,
                              void* workspace, void* stream) {
+  omni_begin();
   OMNI_CHECK(n_vision >= 1, OMNI_E_LAYOUT, "probe keys need at least one vision token");
   OMNI_CHECK(n_vision <= seq_len, OMNI_E_LAYOUT, "n_vision exceeds seq_len");
   OMNI_CHECK(sink_index >= 0 && sink_index < seq_len, OMNI_E_LAYOUT, "sink_index outside the sequence");
@@ -554,6 +581,11 @@ extern "C" int omni_kv_probe(const void* K, int dtype, int n_kv_heads, int seq_l
                                                     block_size, pooled_k, vis);
     probe_finish_kernel<float><<<dim3((head_dim + 31) / 32, n_kv_heads), 1024, 0, s>>>(static_cast<const float*>(K), seq_len, head_dim, nb,
                                                            n_vision, sink_index, vis, k_lazy, k_act);
+  } else if (dtype == OMNI_DTYPE_F64) {
+    kv_probe_kernel<double><<<grid, 256, shm, s>>>(static_cast<const double*>(K), seq_len, head_dim, n_vision,
+                                                     block_size, pooled_k, vis);
+    probe_finish_kernel<double><<<dim3((head_dim + 31) / 32, n_kv_heads), 1024, 0, s>>>(
+        static_cast<const double*>(K), seq_len, head_dim, nb, n_vision, sink_index, vis, k_lazy, k_act);
   } else {
     OMNI_CHECK(false, OMNI_E_PARAM, "unsupported dtype");
   }
@@ -564,6 +596,7 @@ extern "C" int omni_q_score(const void* Q, int dtype, int n_q_heads, int n_kv_he
                             int n_vision, double tau, int preserve_first_head, int block_size, const double* k_lazy,
                             const double* k_act, uint8_t* active, double* p_act, double* pooled_q,
                             int32_t* block_active, void* O_zero, void* stream) {
+  omni_begin();
   OMNI_CHECK(tau >= 0.0 && tau < 1.0, OMNI_E_PARAM, "tau must be in [0, 1)");
   OMNI_CHECK(block_size >= 1, OMNI_E_PARAM, "block size must be >= 1");
   OMNI_CHECK(n_vision >= 0 && n_vision <= seq_len, OMNI_E_LAYOUT, "n_vision outside the sequence");
@@ -577,11 +610,7 @@ extern "C" int omni_q_score(const void* Q, int dtype, int n_q_heads, int n_kv_he
   __nv_bfloat16* oz = static_cast<__nv_bfloat16*>(O_zero);
   if (dtype == OMNI_DTYPE_BF16 && head_dim == 128 && block_size >= 64 && block_size <= QSB_MAX_ROWS) {
     const int shm = block_size * head_dim * 2;
-    static int attr = 0;
-    if (shm > attr) {
-      OMNI_CUDA_TRY(cudaFuncSetAttribute(q_score_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, shm));
-      attr = shm;
-    }
+    OMNI_CUDA_TRY(omni_smem_attr(q_score_bulk_kernel, QSB_MAX_ROWS * 128 * 2));  // one limit for every block size
     q_score_bulk_kernel<<<grid, 256, shm, s>>>(static_cast<const __nv_bfloat16*>(Q), seq_len, rep, n_vision, tau, T,
                                                preserve_first_head, block_size, k_lazy, k_act, active, p_act, pooled_q,
                                                block_active, oz);
@@ -593,6 +622,10 @@ extern "C" int omni_q_score(const void* Q, int dtype, int n_q_heads, int n_kv_he
     q_score_kernel<float><<<grid, 256, 0, s>>>(static_cast<const float*>(Q), seq_len, head_dim, rep, n_vision, tau, T,
                                                preserve_first_head, block_size, k_lazy, k_act, active, p_act,
                                                pooled_q, block_active, oz);
+  else if (dtype == OMNI_DTYPE_F64)
+    q_score_kernel<double><<<grid, 256, 0, s>>>(static_cast<const double*>(Q), seq_len, head_dim, rep, n_vision, tau,
+                                                T, preserve_first_head, block_size, k_lazy, k_act, active, p_act,
+                                                pooled_q, block_active, oz);
   else
     OMNI_CHECK(false, OMNI_E_PARAM, "unsupported dtype");
   return omni_launch_check();
@@ -600,6 +633,7 @@ extern "C" int omni_q_score(const void* Q, int dtype, int n_q_heads, int n_kv_he
 
 extern "C" int omni_compact_rows(const uint8_t* active, const int32_t* block_active, int n_q_heads, int seq_len,
                                  int block_size, int32_t* rows, int32_t* counts, void* stream) {
+  omni_begin();
   OMNI_CHECK(block_size >= 1, OMNI_E_PARAM, "block size must be >= 1");
   dim3 grid(nblocks(seq_len, block_size), n_q_heads);
   compact_rows_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(active, block_active, seq_len, block_size,
@@ -610,8 +644,9 @@ extern "C" int omni_compact_rows(const uint8_t* active, const int32_t* block_act
 extern "C" int omni_gather_rows(const void* src, int dtype, int n_groups, int src_rows, int head_dim,
                                 const int32_t* idx, int idx_stride, const int32_t* counts, int count_const, void* dst,
                                 int dst_rows, int pad_rows, void* stream) {
+  omni_begin();
   OMNI_CHECK(pad_rows >= 1, OMNI_E_PARAM, "pad_rows must be >= 1");
-  const int esz = dtype == OMNI_DTYPE_BF16 ? 2 : 4;
+  const int esz = dtype == OMNI_DTYPE_BF16 ? 2 : dtype == OMNI_DTYPE_F64 ? 8 : 4;
   const int row_bytes = head_dim * esz;
   OMNI_CHECK(row_bytes % 16 == 0, OMNI_E_SHAPE, "row bytes must be a multiple of 16");
   dim3 grid(nblocks(dst_rows, 8 * GR_ROWS), n_groups);
@@ -625,7 +660,8 @@ extern "C" int omni_gather_rows(const void* src, int dtype, int n_groups, int sr
 extern "C" int omni_scatter_rows(const void* src, int dtype, int n_groups, int src_rows, int head_dim,
                                  const int32_t* idx, int idx_stride, const int32_t* counts, void* dst, int dst_rows,
                                  void* stream) {
-  const int esz = dtype == OMNI_DTYPE_BF16 ? 2 : 4;
+  omni_begin();
+  const int esz = dtype == OMNI_DTYPE_BF16 ? 2 : dtype == OMNI_DTYPE_F64 ? 8 : 4;
   const int row_bytes = head_dim * esz;
   OMNI_CHECK(row_bytes % 16 == 0, OMNI_E_SHAPE, "row bytes must be a multiple of 16");
   OMNI_CHECK(counts != nullptr, OMNI_E_PARAM, "scatter needs device counts");
@@ -645,6 +681,7 @@ extern "C" int omni_scatter_rows(const void* src, int dtype, int n_groups, int s
 extern "C" int omni_slim_cache(const void* K, const void* V, int dtype, int n_kv_heads, int seq_len, int head_dim,
                                const int32_t* vision_selected, int sel_stride, int budget, int vcap, void* vision_k,
                                void* vision_v, void* stream) {
+  omni_begin();
   OMNI_CHECK(budget >= 1 && budget <= vcap, OMNI_E_INTEGRITY, "budget outside [1, vision capacity]");
   int rc = omni_gather_rows(K, dtype, n_kv_heads, seq_len, head_dim, vision_selected, sel_stride, nullptr, budget,
                             vision_k, vcap, vcap, stream);

@@ -4,7 +4,8 @@
 Vectors are per-token scores (NumPy or torch); they are handed to the kernel
 as ``block_size = 1`` column masses, so the same kernel that runs the 64K
 probe path (block-constant scores) computes token-exact kurtosis, budget and
-top-b here (vectors up to 8192 tokens; the probe path covers longer ones).
+top-b here, in the reference's arithmetic order (module docstring of
+``csrc/select.cu``): bit-exact with the reference on identical vectors.
 """
 
 from __future__ import annotations
@@ -145,19 +146,18 @@ def select_vision_keys(scores: KeyScores, budget: int, n_vision: int) -> Selecti
 def select_top_blocks(scores: KeyScores, budget: int, block_size: int) -> SelectionResult:
     """kv_select.py:147-176: whole blocks ranked by summed token mass (ties to
     the lower block), the marginal block contributing its lowest indices —
-    exactly ``budget`` keys per head. The block sums are the reference's
-    np.add.reduceat; ranking and the block table run on the GPU (K3b)."""
+    exactly ``budget`` keys per head. Block sums (np.add.reduceat order),
+    ranking and the block table all run on the GPU (omni_block_sums,
+    omni_top_blocks)."""
     n = scores.num_keys
     if not 1 <= budget <= n:
         raise ParameterError(f"budget must be in [1, {n}], got {budget}")
     if block_size < 1:
         raise ParameterError(f"block size must be >= 1, got {block_size}")
-    starts = np.arange(0, n, block_size)
-    bm = np.stack([np.add.reduceat(np.asarray(a.cpu() if isinstance(a, torch.Tensor) else a, dtype=np.float64),
-                                   starts) for a in scores.scores])
-    h = bm.shape[0]
-    sel = ops.select(torch.from_numpy(bm).to("cuda"), h, n, block_size, 0.5, "block", budget_override=budget)
-    s = sel.selected.cpu().numpy()
+    h = scores.num_heads
+    bm = ops.block_sums(_mass(scores.scores), block_size)  # np.add.reduceat order, on the device
+    sel, _ = ops.top_blocks(bm, n, block_size, budget)
+    s = sel.cpu().numpy()
     return SelectionResult(budget, [s[g, :budget].astype(np.int64) for g in range(h)], flattest_head(scores))
 
 

@@ -23,7 +23,7 @@ from . import _lib
 from .errors import ParameterError, ShapeError
 
 GRAN = {"token": 0, "block": 1}
-DTYPE = {torch.bfloat16: 0, torch.float32: 1}
+DTYPE = {torch.bfloat16: 0, torch.float32: 1, torch.float64: 2}
 TILE = 128  # attention tile rows / key tile (K_sel padding)
 
 
@@ -37,7 +37,7 @@ def _stream():
 
 def _dtype(t: torch.Tensor) -> int:
     if t.dtype not in DTYPE:
-        raise ShapeError(f"unsupported dtype {t.dtype}; use bfloat16 or float32")
+        raise ShapeError(f"unsupported dtype {t.dtype}; use bfloat16, float32 or float64")
     return DTYPE[t.dtype]
 
 
@@ -138,7 +138,7 @@ class Selection:
 
     selected: torch.Tensor      # i32 [Hkv, N]; first `counts[g]` entries valid, ascending
     info: torch.Tensor          # i32 [4 + Hkv] = budget, flattest, Hkv, nb, counts...
-    stats: torch.Tensor         # f64 [Hkv + 2] = kurtoses..., retained, total
+    stats: torch.Tensor         # f64 [Hkv + 4] = kurtoses..., retained, total, margin, replayed
     group_scores: torch.Tensor  # f64 [Hkv, nb] per-token score of each block
 
     @property
@@ -155,11 +155,50 @@ def select(mass: torch.Tensor, n_kv_heads: int, seq_len: int, block_size: int, p
     dev = mass.device
     selected = torch.empty(n_kv_heads, seq_len, device=dev, dtype=torch.int32)
     info = torch.empty(4 + n_kv_heads, device=dev, dtype=torch.int32)
-    stats = torch.empty(n_kv_heads + 2, device=dev, dtype=torch.float64)
+    stats = torch.empty(n_kv_heads + 4, device=dev, dtype=torch.float64)
     gs = torch.empty(n_kv_heads, nb, device=dev, dtype=torch.float64)
-    _lib.call("omni_select", _p(mass), hq, n_kv_heads, seq_len, block_size, float(p), GRAN[granularity],
-              int(vision_limit), int(budget_override), _p(selected), _p(info), _p(stats), _p(gs), _stream())
+    wsb = _lib.size("omni_select_workspace", n_kv_heads, seq_len, block_size)
+    ws = torch.empty(wsb, device=dev, dtype=torch.uint8) if wsb else None
+    _lib.call("omni_select_ex", _p(mass.contiguous()), hq, n_kv_heads, seq_len, block_size, float(p),
+              GRAN[granularity], int(vision_limit), int(budget_override), _p(selected), _p(info), _p(stats), _p(gs),
+              _p(ws), _stream())
     return Selection(selected, info, stats, gs)
+
+
+def block_sums(x: torch.Tensor, block_size: int) -> torch.Tensor:
+    """np.add.reduceat(x[r], arange(0, n, block_size)) per row, in NumPy's
+    order (omni_block_sums; kv_select.py:160)."""
+    if x.dtype != torch.float64 or not x.is_cuda or x.dim() != 2:
+        raise ShapeError("block_sums takes a CUDA float64 [rows, n] tensor")
+    x = x.contiguous()
+    rows, n = x.shape
+    out = torch.empty(rows, n_blocks(n, block_size), device=x.device, dtype=torch.float64)
+    _lib.call("omni_block_sums", _p(x), rows, n, int(block_size), _p(out), _stream())
+    return out
+
+
+def top_blocks(block_mass: torch.Tensor, seq_len: int, block_size: int, budget: int):
+    """select_top_blocks' table from block masses [G, nb] (omni_top_blocks):
+    returns (selected i32 [G, seq_len], counts i32 [G])."""
+    if block_mass.dtype != torch.float64 or not block_mass.is_cuda or block_mass.dim() != 2:
+        raise ShapeError("top_blocks takes CUDA float64 block masses [groups, blocks]")
+    bm = block_mass.contiguous()
+    g = bm.shape[0]
+    selected = torch.empty(g, seq_len, device=bm.device, dtype=torch.int32)
+    info = torch.zeros(4 + g, device=bm.device, dtype=torch.int32)
+    ws = torch.empty(_lib.size("omni_top_blocks_workspace", g, seq_len, block_size), device=bm.device,
+                     dtype=torch.uint8)
+    _lib.call("omni_top_blocks", _p(bm), g, seq_len, int(block_size), int(budget), _p(selected), _p(info), _p(ws),
+              _stream())
+    return selected, info[4:]
+
+
+def probe_map(ws: torch.Tensor, n_q_heads: int, nb: int) -> torch.Tensor:
+    """The normalised block-causal probe map [Hq, nb, nb] from the workspace
+    of ``probe_mass(..., return_workspace=True)`` (omni_probe_map)."""
+    out = torch.empty(n_q_heads, nb, nb, device=ws.device, dtype=torch.float64)
+    _lib.call("omni_probe_map", _p(ws), n_q_heads, nb, _p(out), _stream())
+    return out
 
 
 # ----------------------------------------------------------------------- K6
@@ -205,6 +244,9 @@ def scatter_rows(src: torch.Tensor, idx: torch.Tensor, counts: torch.Tensor, out
 
 
 # ----------------------------------------------------------------------- K4
+last_fwd_status: torch.Tensor | None = None
+
+
 def sparse_attn_fwd(Q, K_sel, V_sel, V, rows, counts, selected, sel_counts, sink_index: int,
                     O: torch.Tensor, lse: torch.Tensor | None = None):
     """tcgen05 sparse flash-attention forward into O (lazy rows untouched)."""
@@ -214,24 +256,15 @@ def sparse_attn_fwd(Q, K_sel, V_sel, V, rows, counts, selected, sel_counts, sink
         raise ShapeError("sparse attention consumes bf16 Q/K/V")
     if selected.shape[-1] != n:
         raise ShapeError("selected must be [Hkv, N]")
+    # the fast kernel's overflow status word (caller-owned workspace, zeroed
+    # by the call itself): one per call from the stream-ordered caching
+    # allocator, so concurrent forwards on different streams never share it
+    global last_fwd_status
+    status = torch.empty(1, device=Q.device, dtype=torch.int32)
+    last_fwd_status = status  # diagnostics only (tests read whether the safe re-run fired)
     _lib.call("omni_sparse_attn_fwd_ex", _p(Q), _p(K_sel), _p(V_sel), _p(V), _p(rows), _p(counts), _p(selected),
-              _p(sel_counts), hq, hkv, n, d, cap, sink_index, _p(O), _p(lse), _p(_status_word(Q.device)), _stream())
+              _p(sel_counts), hq, hkv, n, d, cap, sink_index, _p(O), _p(lse), _p(status), _stream())
     return O, lse
-
-
-_STATUS: dict = {}
-
-
-def _status_word(device) -> torch.Tensor:
-    """Per-device int32 status word of the fast forward kernel (caller-owned
-    workspace of omni_sparse_attn_fwd_ex; allocated once per device)."""
-    device = torch.device(device)
-    if device.index is None:
-        device = torch.device(device.type, torch.cuda.current_device())
-    key = str(device)
-    if key not in _STATUS:
-        _STATUS[key] = torch.zeros(1, device=device, dtype=torch.int32)
-    return _STATUS[key]
 
 
 def sparse_attn_bwd(Q, K_sel, V_sel, O, dO, lse, rows, counts, selected, sel_counts, dq_dtype=torch.float32):
@@ -255,58 +288,71 @@ def sparse_attn_bwd(Q, K_sel, V_sel, O, dO, lse, rows, counts, selected, sel_cou
 
 
 # ----------------------------------------------------------------------- K7
-def decode_step(q, vision_k, vision_v, vision_len, text_k, text_v, n_text: int, answer_k, answer_v, n_answer: int,
-                k_lazy, k_act, tau: float, preserve_first_head: bool, flags_override=None, out=None, flags=None):
-    """One batched slim-cache decode step (decode.py:124-194, rule B)."""
+def decode_paged(q, pool_k, pool_v, table, vision_len, text_len, answer_len, n_chunks: int, k_lazy, k_act,
+                 tau: float, preserve_first_head: bool, status, head_dim: int | None = None, flags_override=None,
+                 out=None, flags=None):
+    """One batched decode step over the paged slim cache (omni_decode;
+    decode.py:124-194, rule B). ``head_dim``: logical width of rows
+    zero-padded to the 128-column storage (softmax scale 1/sqrt(head_dim))."""
     b, hq, d = q.shape
-    hkv, vcap = vision_k.shape[1], vision_k.shape[2]
-    acap = answer_k.shape[2]
+    hkv = table.shape[1]
     dev = q.device
     if out is None:
         out = torch.empty(b, hq, d, device=dev, dtype=torch.float32)
     if flags is None:
         flags = torch.empty(b, hq, device=dev, dtype=torch.uint8)
-    ws = torch.empty(_lib.size("omni_decode_workspace", b, hq, vcap, n_text, acap, d), device=dev, dtype=torch.uint8)
-    _lib.call("omni_decode_step", _p(q), _p(vision_k), _p(vision_v), _p(vision_len), _p(text_k), _p(text_v), n_text,
-              _p(answer_k), _p(answer_v), n_answer, _p(k_lazy), _p(k_act), b, hq, hkv, d, vcap, acap, float(tau),
-              int(bool(preserve_first_head)), _p(flags_override), _p(flags), _p(out), _p(ws), _stream())
+    ws = torch.empty(_lib.size("omni_decode_workspace", b, hq, n_chunks), device=dev, dtype=torch.uint8)
+    _lib.call("omni_decode", _p(q), _p(pool_k), _p(pool_v), pool_k.shape[0], _p(table), table.shape[2],
+              _p(vision_len), _p(text_len), _p(answer_len), int(n_chunks), _p(k_lazy), _p(k_act), b, hq, hkv,
+              head_dim or d, float(tau), int(bool(preserve_first_head)), _p(flags_override), _p(flags), _p(out),
+              _p(ws), _p(status), _stream())
     return out, flags
 
 
-def decode_step_varlen(q, vision_k, vision_v, vision_len, text_k, text_v, text_len, answer_k, answer_v, answer_len,
-                       k_lazy, k_act, tau: float, preserve_first_head: bool, status, flags_override=None, out=None,
-                       flags=None):
-    """K7 over a ragged batch: per-sequence text / answer lengths (device i32
-    [B]); ``status`` (device i32 [1]) receives the degenerate-context flag."""
-    b, hq, d = q.shape
-    hkv, vcap = vision_k.shape[1], vision_k.shape[2]
-    tcap, acap = text_k.shape[2], answer_k.shape[2]
-    dev = q.device
-    if out is None:
-        out = torch.empty(b, hq, d, device=dev, dtype=torch.float32)
-    if flags is None:
-        flags = torch.empty(b, hq, device=dev, dtype=torch.uint8)
-    ws = torch.empty(_lib.size("omni_decode_workspace", b, hq, vcap, tcap, acap, d), device=dev, dtype=torch.uint8)
-    _lib.call("omni_decode_step_varlen", _p(q), _p(vision_k), _p(vision_v), _p(vision_len), _p(text_k), _p(text_v),
-              _p(text_len), tcap, _p(answer_k), _p(answer_v), _p(answer_len), _p(k_lazy), _p(k_act), b, hq, hkv, d,
-              vcap, acap, float(tau), int(bool(preserve_first_head)), _p(flags_override), _p(flags), _p(out), _p(ws),
-              _p(status), _stream())
-    return out, flags
-
-
-def append_answer(k_rows, v_rows, answer_k, answer_v, n_answer: int, answer_len=None) -> None:
-    """One launch for the batch's new answer K / V rows (omni_append_answer)."""
+def append_answer_paged(k_rows, v_rows, pool_k, pool_v, table, vision_len, text_len, answer_len) -> None:
+    """One launch for the batch's new answer K / V rows (omni_append_answer):
+    row answer_len[s] of every (sequence, group), answer_len advanced on the
+    device. The rows' pages must be in the table already."""
     b, hkv, d = k_rows.shape
-    kb = k_rows if k_rows.dtype == torch.bfloat16 else k_rows.to(torch.bfloat16)
-    vb = v_rows if v_rows.dtype == torch.bfloat16 else v_rows.to(torch.bfloat16)
-    _lib.call("omni_append_answer", _p(kb.contiguous()), _p(vb.contiguous()), _p(answer_k), _p(answer_v), b, hkv, d,
-              answer_k.shape[2], int(n_answer), _p(answer_len), _stream())
+    for name, t in (("k_rows", k_rows), ("v_rows", v_rows)):
+        if not t.is_cuda or t.device != pool_k.device:
+            raise ShapeError(f"{name} must be a CUDA tensor on the cache's device")
+    # bind the converted rows to locals: they must outlive the (asynchronous)
+    # append kernel, or the allocator could hand K's temporary to V's copy
+    kb = k_rows.to(torch.bfloat16).contiguous()
+    vb = v_rows.to(torch.bfloat16).contiguous()
+    _lib.call("omni_append_answer", _p(kb), _p(vb), _p(pool_k), _p(pool_v), _p(table), table.shape[2],
+              _p(vision_len), _p(text_len), _p(answer_len), b, hkv, d, _stream())
 
 
-def call_decode_flags(q, k_lazy, k_act, n_kv_heads: int, tau: float, preserve_first_head: bool, flags) -> None:
+def page_write(src: torch.Tensor, idx, count: int, table_rows: torch.Tensor, first_slot: int,
+               pool: torch.Tensor) -> None:
+    """Rows of src [G, rows, 128] bf16 (gathered by idx [G, >= count] when
+    given) into the pages table_rows[g, first_slot + r / 64] of ``pool``
+    (omni_page_write); the last page's tail is zero-filled."""
+    _cuda3(src, "src")
+    g, rows, d = src.shape
+    if src.dtype != torch.bfloat16 or pool.dtype != torch.bfloat16:
+        raise ShapeError("pages hold bf16 rows")
+    tr = table_rows.contiguous()
+    _lib.call("omni_page_write", _p(src), g, rows, d, _p(idx), idx.shape[-1] if idx is not None else 0, int(count),
+              _p(tr), tr.shape[-1], int(first_slot), _p(pool), _stream())
+
+
+def call_decode_flags(q, k_lazy, k_act, n_kv_heads: int, tau: float, preserve_first_head: bool, flags,
+                      head_dim: int | None = None) -> None:
     b, hq, d = q.shape
-    _lib.call("omni_decode_flags", _p(q), _p(k_lazy), _p(k_act), b, hq, n_kv_heads, d, float(tau),
+    _lib.call("omni_decode_flags", _p(q), _p(k_lazy), _p(k_act), b, hq, n_kv_heads, head_dim or d, float(tau),
               int(bool(preserve_first_head)), _p(flags), _stream())
+
+
+def decode_flags_f64(q, k_lazy, k_act, n_kv_heads: int, tau: float, preserve_first_head: bool, flags) -> None:
+    """classify_decode_query on float64 queries [B, Hq, d] (omni_decode_flags_f64)."""
+    if q.dtype != torch.float64 or not q.is_cuda:
+        raise ShapeError("decode_flags_f64 takes CUDA float64 queries")
+    b, hq, d = q.shape
+    _lib.call("omni_decode_flags_f64", _p(q.contiguous()), _p(k_lazy), _p(k_act), b, hq, n_kv_heads, d,
+              k_lazy.shape[-1], float(tau), int(bool(preserve_first_head)), _p(flags), _stream())
 
 
 def device_check() -> None:

@@ -77,7 +77,7 @@ def select_device(Q: torch.Tensor, K: torch.Tensor, n_vision: int, cfg: Sparsity
 
     score_source "probe" (hot path): block-probe column masses (K3a).
     score_source "exact": column masses of the full causal maps (K3x, O(N^2 d)
-    float64; N <= 8192 for the token-level selection)."""
+    float64) and a token-level selection (the general K3b path)."""
     hq, n, d = Q.shape
     if not 1 <= n_vision <= n:
         raise LayoutError(f"n_vision {n_vision} outside [1, {n}]")
@@ -95,16 +95,14 @@ def select_device(Q: torch.Tensor, K: torch.Tensor, n_vision: int, cfg: Sparsity
     else:
         mass = ops.exact_mass(Q, K)
         sel = ops.select(mass, K.shape[0], n, 1, cfg.p, "token")
-        if cfg.granularity == "block":  # select_top_blocks over the same budget (kv_select.py:147-176)
-            nb = ops.n_blocks(n, cfg.block_size)
-            pad = nb * cfg.block_size - n
-            blk = torch.nn.functional.pad(mass, (0, pad)).view(hq, nb, cfg.block_size).sum(dim=2)
-            bsel = ops.select(blk, K.shape[0], n, cfg.block_size, cfg.p, "block",
-                              budget_override=int(sel.info[0]))
-            bsel.info[1] = sel.info[1]
-            bsel.stats[: K.shape[0]] = sel.stats[: K.shape[0]]
-            bsel.stats[K.shape[0]:] = sel.stats[K.shape[0]:]
-            sel = bsel
+        if cfg.granularity == "block":
+            # select_top_blocks over the same budget (prefill.py:168-169,
+            # kv_select.py:147-176): np.add.reduceat block sums of the
+            # token-level group scores, ranked on the device; the key scores
+            # and kurtoses stay token-level, as the reference returns them
+            blk = ops.block_sums(sel.group_scores, cfg.block_size)
+            sel.selected, bcounts = ops.top_blocks(blk, n, cfg.block_size, int(sel.info[0]))
+            sel.info[4:] = bcounts
     return k_lazy, k_act, pk, active, p_act, pq, rows, counts, mass, sel
 
 

@@ -59,11 +59,13 @@ def sparse_prefill(w: AttentionWorkload, cfg: SparsityConfig = SparsityConfig(),
     """Query masks -> probe key scores -> flattest-group budget -> per-group
     top-b -> sparse attention (reference prefill.py:142-192 under rule B).
     The block-probe score source is the hot path; "exact" computes the
-    dense causal maps' column masses on the GPU (K3x, O(N^2 d) float64,
-    N <= 8192) without materialising them."""
+    dense causal maps' column masses on the GPU (K3x, O(N^2 d) float64)
+    without materialising them."""
     if score_source not in SCORE_SOURCES:
         raise ParameterError(f"score source must be one of {SCORE_SOURCES}")
-    Q, K, V = w.device_tensors()
+    # selection in the caller's precision (float64 for the reference's own
+    # arrays), attention on bf16 copies (sparse_prefill_device converts)
+    Q, K, V = w.device_tensors(w.source_dtype())
     res = sparse_prefill_device(Q, K, V, w.layout.n_vision, SparsityConfig(
         tau=cfg.tau, p=cfg.p, block_size=cfg.block_size, granularity=cfg.granularity,
         preserve_first_head=cfg.preserve_first_head, sink_index=w.layout.sink_index), score_source=score_source)
@@ -82,7 +84,8 @@ def sparse_prefill(w: AttentionWorkload, cfg: SparsityConfig = SparsityConfig(),
     if with_recall:
         from .metrics import attention_recall_device
 
-        recall = attention_recall_device(res, Q, K, V, w.layout.sink_index).cpu().tolist()
+        bf = lambda t: t.to(torch.bfloat16).contiguous()
+        recall = attention_recall_device(res, bf(Q), bf(K), bf(V), w.layout.sink_index).cpu().tolist()
     return PrefillOutput(outs, masks, SelectionResult(b, selected, flat), list(stats[:hkv]), float(stats[hkv]),
                          float(stats[hkv + 1]), score_source, res, KeyScores(scores, list(stats[:hkv])), recall)
 

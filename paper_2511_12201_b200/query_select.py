@@ -1,7 +1,7 @@
 """Reference-named query-selection operators on the GPU (reference
 ``query_select.py:22-92``) over K1 ``omni_kv_probe`` and K2 ``omni_q_score``.
-NumPy in -> NumPy out, like the reference; all arithmetic is float64 on the
-device."""
+NumPy in -> NumPy out, like the reference; float64 inputs stay float64 and
+all arithmetic is float64 on the device."""
 
 from __future__ import annotations
 
@@ -34,9 +34,13 @@ class QueryMask:
         return int(self.active.sum())
 
 
-def _dev(x, dtype=torch.float32) -> torch.Tensor:
-    t = x if isinstance(x, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(np.asarray(x, dtype=np.float32)))
-    return t.to(device="cuda", dtype=dtype).contiguous()
+def _dev(x) -> torch.Tensor:
+    """Device copy in the caller's precision (float64 NumPy arrays stay
+    float64, as the reference computes; fp32 / bf16 tensors keep theirs)."""
+    t = x if isinstance(x, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(np.asarray(x)))
+    if t.dtype not in (torch.float64, torch.float32, torch.bfloat16):
+        t = t.to(torch.float64)
+    return t.to(device="cuda").contiguous()
 
 
 def build_probe_keys(k, layout: TokenLayout) -> ProbeKeys:
@@ -66,7 +70,7 @@ def build_query_masks(w: AttentionWorkload, tau: float, preserve_first_head: boo
     text/answer rows active, head 0 forced active (query_select.py:71-92)."""
     if not 0.0 <= tau < 1.0:
         raise ValueError(f"tau must be in [0, 1), got {tau}")
-    Q, K, _ = w.device_tensors(torch.float32)
+    Q, K, _ = w.device_tensors(w.source_dtype())
     nv = w.layout.n_vision
     kl, ka, _ = ops.kv_probe(K, nv, w.layout.sink_index, 256)
     active, _, _, _ = ops.q_score(Q, kl, ka, nv, tau, preserve_first_head, 256)

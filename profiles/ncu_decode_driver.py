@@ -12,11 +12,11 @@ for s in range(B):
     k_lazy, k_act, _, _, _, _, _, _, mass, sel = select_device(Q, K, nv, cfg)
     b = min(int(sel.info[0]), nv)
     vsel = ops.select(mass, HKV, n, 256, cfg.p, "token", vision_limit=nv, budget_override=b)
-    caches.append(gdec.build_cache(K, V, vsel.selected, b, nv, 64, k_lazy, k_act, HQ, answer_capacity=16))
+    caches.append(gdec.build_cache_device(K, V, vsel.selected, b, nv, 64, k_lazy, k_act, HQ, answer_capacity=16))
     means.append(unit_vision_mean(K, nv))
     del Q, K, V
 cache = gdec.stack_caches(caches); del caches
 for t in range(3):
     q = decode_queries_device(HQ, HKV, means, range(B), 0.5, t)
-    gdec.decode_attention(q, cache, cfg.tau, log=False)
+    gdec.decode_attention_batch(q, cache, cfg.tau, log=False)
 torch.cuda.synchronize()

@@ -157,14 +157,12 @@ def test_select_top_blocks_sparsity_gap_and_decode_classification():
     q = torch.randn(3, hq, d, device="cuda").to(torch.bfloat16)
     k_lazy = torch.randn(3, hkv, d, device="cuda", dtype=torch.float64)
     k_act = torch.randn(3, hkv, d, device="cuda", dtype=torch.float64)
-    cache = gdec.SlimKVCache(*(torch.zeros(3, hkv, 128, d, device="cuda", dtype=torch.bfloat16) for _ in range(2)),
-                             torch.full((3,), 64, device="cuda", dtype=torch.int32),
-                             torch.zeros(3, hkv, 128, device="cuda", dtype=torch.int32),
-                             *(torch.randn(3, hkv, 16, d, device="cuda").to(torch.bfloat16) for _ in range(2)),
-                             *(torch.zeros(3, hkv, 4, d, device="cuda", dtype=torch.bfloat16) for _ in range(2)),
-                             k_lazy, k_act, hq, True, budgets=[64] * 3)
-    fl = gdec.classify_decode_query(q, cache, 0.3).cpu().numpy().astype(bool)
-    _, fl2 = gdec.decode_attention(q, cache, 0.3, log=False)
+    K = torch.randn(hkv, 200, d, device="cuda").to(torch.bfloat16)
+    sel = torch.arange(64, device="cuda", dtype=torch.int32).repeat(hkv, 1)
+    caches = [gdec.build_cache_device(K, K, sel, 64, 184, 16, k_lazy[s], k_act[s], hq) for s in range(3)]
+    cache = gdec.stack_caches(caches)
+    fl = gdec.classify_decode_batch(q, cache, 0.3).cpu().numpy().astype(bool)
+    _, fl2 = gdec.decode_attention_batch(q, cache, 0.3, log=False)
     np.testing.assert_array_equal(fl, fl2.cpu().numpy().astype(bool))
     for s in range(3):
         for h in range(hq):

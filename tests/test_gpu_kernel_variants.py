@@ -38,7 +38,7 @@ for h in (0, 3, 4, 7):
     fin = np.isfinite(el[act])
     err = max(err, float(np.max(np.abs(lse[h][act][fin] - el[act][fin]))) / 0.02)
 from paper_2511_12201_b200 import ops
-status = int(ops._status_word(torch.device("cuda"))[0])
+status = int(ops.last_fwd_status[0])
 print(json.dumps({"scaled_err": err, "nan": bool(np.isnan(out).any()), "fallback": status}))
 """
 

@@ -229,21 +229,32 @@ def test_exact_score_source_c1_end_to_end():
 @pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
 def test_q_score_decision_at_the_boundary(dtype):
     """K2 decides far from the boundary on l1 - l0 vs ln(tau/(1-tau)) and
-    evaluates the reference expression (query_select.py:63-68) near it. With
-    tau set to rows' own computed p_act (the hardest ties: p > tau is false
-    for exactly those rows), the flags equal p > tau for every row."""
+    evaluates the reference expression (query_select.py:63-68) near it. tau
+    is set to the ORACLE's p_act of sample rows (the hardest ties). Every row
+    whose oracle p is farther from tau than the measured GPU-vs-oracle p
+    difference gets the oracle's verdict; the only rows allowed to differ are
+    those within that arithmetic difference of tau (the tie rows themselves)."""
     from paper_2511_12201_b200 import ops
 
     Q, K, V = generate(Spec(heads=4, heads_kv=2, head_dim=128, n_vision=3000, n_text=40, seed=11))
-    Qd, Kd = to_dev(round_bf16(Q), dtype), to_dev(round_bf16(K), dtype)
+    Qr, Kr = round_bf16(Q), round_bf16(K)
+    Qd, Kd = to_dev(Qr, dtype), to_dev(Kr, dtype)
     kl, ka, _ = ops.kv_probe(Kd, 3000, 0, 256)
     _, p, _, _ = ops.q_score(Qd, kl, ka, 3000, 0.08, False, 256, want_prob=True)
     p = p.cpu().numpy()
+    ref = opipe.select(Qr, Kr, 3000, 0, 0.08, 0.82, 256, preserve_first_head=False)
+    p_ref = ref.p_act
+    diff = float(np.max(np.abs(p - p_ref)))
+    assert diff < 1e-12
     for r in (5, 777, 2999):
-        tau = float(p[1, r])
+        tau = float(p_ref[1, r])
         if not 0.0 < tau < 1.0:
             continue
         act, _, _, _ = ops.q_score(Qd, kl, ka, 3000, tau, False, 256)
         got = act.cpu().numpy()[:, :3000].astype(bool)
-        np.testing.assert_array_equal(got, p > tau)
-        assert not got[1, r]
+        exp = p_ref > tau
+        clear = np.abs(p_ref - tau) > 2 * diff
+        np.testing.assert_array_equal(got[clear], exp[clear])
+        # rows in the ambiguous band: the GPU's verdict is its own p > tau
+        np.testing.assert_array_equal(got[~clear], p[~clear] > tau)
+        assert int((~clear).sum()) <= 4

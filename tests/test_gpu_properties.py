@@ -70,7 +70,7 @@ def test_c5_decode_64k_matches_fp32_reference():
         k_lazy, k_act, _, _, _, _, _, _, mass, sel = select_device(Q, K, nv, cfg)
         b = min(int(sel.info[0]), nv)
         vsel = ops.select(mass, hkv, n, 256, cfg.p, "token", vision_limit=nv, budget_override=b)
-        caches.append(gdec.build_cache(K, V, vsel.selected, b, nv, nt, k_lazy, k_act, hq, answer_capacity=8))
+        caches.append(gdec.build_cache_device(K, V, vsel.selected, b, nv, nt, k_lazy, k_act, hq, answer_capacity=8))
         means.append(unit_vision_mean(K, nv))
         del Q, K, V
     cache = gdec.stack_caches(caches)
@@ -78,7 +78,7 @@ def test_c5_decode_64k_matches_fp32_reference():
     gen.manual_seed(5)
     for t in range(3):
         q = decode_queries_device(hq, hkv, means, [0, 1], 0.5, t)
-        out, fl = gdec.decode_attention(q, cache, cfg.tau)
+        out, fl = gdec.decode_attention_batch(q, cache, cfg.tau)
         rep = hq // hkv
         scale = 1.0 / np.sqrt(d)
         for s in range(2):
@@ -92,16 +92,16 @@ def test_c5_decode_64k_matches_fp32_reference():
                 p_act = 1.0 / (1.0 + np.exp(l0 - l1))
                 exp_flag = bool(p_act > cfg.tau) or h == 0
                 assert bool(fl[s, h]) == exp_flag, (t, s, h, p_act)
-                keys = [cache.text_k[s, g, :nt], cache.answer_k[s, g, :cache.n_answer]]
-                vals = [cache.text_v[s, g, :nt], cache.answer_v[s, g, :cache.n_answer]]
+                keys = [cache.rows(s, g, "text", "k"), cache.rows(s, g, "answer", "k")]
+                vals = [cache.rows(s, g, "text", "v"), cache.rows(s, g, "answer", "v")]
                 if exp_flag:
-                    keys.insert(0, cache.vision_k[s, g, :b])
-                    vals.insert(0, cache.vision_v[s, g, :b])
+                    keys.insert(0, cache.rows(s, g, "vision", "k"))
+                    vals.insert(0, cache.rows(s, g, "vision", "v"))
                 Kc, Vc = torch.cat(keys).float(), torch.cat(vals).float()
                 w = torch.softmax((Kc @ q[s, h].float()) * scale, dim=0)
                 ref = w @ Vc
                 torch.testing.assert_close(out[s, h], ref, atol=5e-3, rtol=2e-2)
-        gdec.append_answer(cache, torch.randn(2, hkv, d, generator=gen, device="cuda"),
+        gdec.append_answer_batch(cache, torch.randn(2, hkv, d, generator=gen, device="cuda"),
                            torch.randn(2, hkv, d, generator=gen, device="cuda"))
 
 

@@ -139,3 +139,58 @@ def test_grad_oracle_forward_pinned_to_sparse_head_attention():
         ref = oatt.sparse_head_attention(Q[h], K[h // 2], V[h // 2], res.selected[h // 2], res.active[h], 0)
         np.testing.assert_allclose(out[h], ref, rtol=1e-12, atol=1e-13)
     assert np.all(dq[~res.active] == 0.0)
+
+
+def _pairwise(a, lo, n):
+    """NumPy's pairwise summation (loops_utils.h.src pairwise_sum) restated
+    in pure Python: the order csrc/select.cu emulates for kurtosis."""
+    if n < 8:
+        r = 0.0
+        for i in range(n):
+            r = r + a[lo + i]
+        return r
+    if n <= 128:
+        r = [a[lo + j] for j in range(8)]
+        i = 8
+        while i < n - (n % 8):
+            for j in range(8):
+                r[j] = r[j] + a[lo + i + j]
+            i += 8
+        res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]))
+        while i < n:
+            res = res + a[lo + i]
+            i += 1
+        return res
+    n2 = n // 2
+    n2 -= n2 % 8
+    return _pairwise(a, lo, n2) + _pairwise(a, lo + n2, n - n2)
+
+
+def test_numpy_summation_orders_the_gpu_emulates():
+    """Pins the arithmetic order K3b reproduces: np.sum is the pairwise sum
+    above for every length, np.add.reduceat sums a segment as its first
+    element plus the pairwise sum of the rest, and the oracle's kurtosis
+    (_core_py.kurtosis) is three pairwise means. Values spread over many
+    binades so that any other order rounds differently."""
+    from oracle.numerics import kurtosis
+
+    rng = np.random.default_rng(0)
+    for n in list(range(1, 260)) + [1000, 1023, 4097, 8193, 65536, 65553, 131072]:
+        a = rng.standard_normal(n) * np.exp(rng.standard_normal(n) * 8)
+        lst = a.tolist()
+        assert np.sum(a) == _pairwise(lst, 0, n), n
+        if n >= 20:
+            starts = np.arange(0, n, 13)
+            r = np.add.reduceat(a, starts)
+            for k in (0, len(starts) // 2, len(starts) - 1):
+                s0 = int(starts[k])
+                m = min(13, n - s0)
+                want = lst[s0] + _pairwise(lst, s0 + 1, m - 1) if m > 1 else lst[s0]
+                assert r[k] == want
+        if n in (1000, 4097, 65553):
+            v = np.abs(a)
+            mu = _pairwise(v.tolist(), 0, n) / n
+            d = [x - mu for x in v.tolist()]
+            m2 = _pairwise([x * x for x in d], 0, n) / n
+            m4 = _pairwise([((x * x) * x) * x for x in d], 0, n) / n
+            assert kurtosis(v) == m4 / (m2 * m2)
