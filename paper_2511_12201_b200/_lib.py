@@ -14,7 +14,10 @@ import os
 from .errors import CudaError, raise_for_status
 
 LIB_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib")
-LIB_PATH = os.path.join(LIB_DIR, "libomnisparse.so")
+# the product library; OMNI_LIBRARY=<path> selects another build of the same
+# ABI (libomnisparse_variants.so: the measured alternative kernels for A/B
+# runs and tests/test_gpu_kernel_variants.py)
+LIB_PATH = os.environ.get("OMNI_LIBRARY") or os.path.join(LIB_DIR, "libomnisparse.so")
 
 _c_int, _c_double, _c_size, _p = ctypes.c_int, ctypes.c_double, ctypes.c_size_t, ctypes.c_void_p
 

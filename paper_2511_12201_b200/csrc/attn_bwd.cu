@@ -366,6 +366,7 @@ dq_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
   }
 }
 
+#ifdef OMNI_VARIANTS  // the shared-memory P^T dkv kernel (v1), kept for A/B measurements
 // ------------------------------------------------------------------ dkv
 namespace dkv {
 constexpr int BR = 64;                     // Q rows per inner tile
@@ -639,6 +640,8 @@ dkv_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUt
     tmem_dealloc(tmem, 512);
   }
 }
+
+#endif  // OMNI_VARIANTS
 
 // ------------------------------------------------------------------ dkv v2
 // dkv with 128-row Q tiles and P^T / dS^T kept in TMEM. Per (key tile, Q
@@ -1068,20 +1071,27 @@ extern "C" int omni_sparse_attn_bwd_ex(const void* Q, const void* K_sel, const v
   if ((rc = omni_make_tmap_rows(&tdo64, dOc, crow, 128, 2, 64, 64))) return rc;
   if ((rc = omni_make_tmap_rows(&tk, K_sel, (uint64_t)n_kv_heads * cap, 128, 2, 64, 128))) return rc;
   if ((rc = omni_make_tmap_rows(&tv, V_sel, (uint64_t)n_kv_heads * cap, 128, 2, 64, 128))) return rc;
-  OMNI_CUDA_TRY(omni_smem_attr(bwd::dq_kernel<0>, (int)bwd::dq::SMEM));
+  const int n_tiles = capq / 128;
+#ifdef OMNI_VARIANTS
   OMNI_CUDA_TRY(omni_smem_attr(bwd::dq_kernel<1>, (int)bwd::dq::SMEM));
   OMNI_CUDA_TRY(omni_smem_attr(bwd::dkv_kernel, (int)bwd::dkv::SMEM));
-  const int n_tiles = capq / 128;
   static const int dq_probe = [] {
     const char* e = getenv("OMNI_DQ_PROBE");
     return e ? atoi(e) : 0;
   }();
-  (dq_probe == 1 ? bwd::dq_kernel<1> : bwd::dq_kernel<0>)<<<n_tiles * n_q_heads, 576, bwd::dq::SMEM, st>>>(tq128, tdo128, tk, tv, rows, counts, lse2c, Dc,
+  auto dq_kern = dq_probe == 1 ? bwd::dq_kernel<1> : bwd::dq_kernel<0>;
+#else
+  auto dq_kern = bwd::dq_kernel<0>;
+#endif
+  OMNI_CUDA_TRY(omni_smem_attr(bwd::dq_kernel<0>, (int)bwd::dq::SMEM));
+  dq_kern<<<n_tiles * n_q_heads, 576, bwd::dq::SMEM, st>>>(tq128, tdo128, tk, tv, rows, counts, lse2c, Dc,
                                                                     visc, n_q_heads, rep, seq_len, cap, capq, n_tiles,
                                                                     dQ, dq_dtype == OMNI_DTYPE_BF16 ? 1 : 0);
   if ((rc = omni_launch_check())) return rc;
+#ifdef OMNI_VARIANTS
   // dkv implementation: TMEM-resident P^T / dS^T kernel by default;
-  // OMNI_BWD_DKV=v1 selects the shared-memory P^T kernel.
+  // OMNI_BWD_DKV=v1 selects the shared-memory P^T kernel, OMNI_BWD_PROBE the
+  // profiling instances of dkv2.
   static const bool dkv_v1 = [] {
     const char* e = getenv("OMNI_BWD_DKV");
     return e && strcmp(e, "v1") == 0;
@@ -1090,23 +1100,29 @@ extern "C" int omni_sparse_attn_bwd_ex(const void* Q, const void* K_sel, const v
     bwd::dkv_kernel<<<dim3(cap / 128, n_kv_heads * rep), 384, bwd::dkv::SMEM, st>>>(
         tq64, tdo64, tk, tv, rows, counts, selected, sel_counts, lse2c, Dc, visc, rep, seq_len, cap, capq, dK_sel,
         dV_sel);
-  } else {
-    static const int probe = [] {
-      const char* e = getenv("OMNI_BWD_PROBE");
-      return e ? atoi(e) : 0;
-    }();
-    auto kern = probe == 1   ? bwd::dkv2_kernel<1>
-                : probe == 2 ? bwd::dkv2_kernel<2>
-                : probe == 3 ? bwd::dkv2_kernel<3>
-                             : bwd::dkv2_kernel<0>;
-    OMNI_CUDA_TRY(omni_smem_attr(kern, (int)bwd::dkv2::SMEM));
-    kern<<<dim3(cap / 128, n_kv_heads * rep), bwd::dkv2::NTHREADS, bwd::dkv2::SMEM, st>>>(
-        tq128, tdo128, tk, tv, rows, counts, selected, sel_counts, lse2c, Dc, visc, rep, seq_len, cap, capq, dK_sel,
-        dV_sel);
+    return omni_launch_check();
   }
+  static const int probe = [] {
+    const char* e = getenv("OMNI_BWD_PROBE");
+    return e ? atoi(e) : 0;
+  }();
+  auto kern = probe == 1   ? bwd::dkv2_kernel<1>
+              : probe == 2 ? bwd::dkv2_kernel<2>
+              : probe == 3 ? bwd::dkv2_kernel<3>
+                           : bwd::dkv2_kernel<0>;
+#else
+  (void)tq64;
+  (void)tdo64;
+  auto kern = bwd::dkv2_kernel<0>;
+#endif
+  OMNI_CUDA_TRY(omni_smem_attr(kern, (int)bwd::dkv2::SMEM));
+  kern<<<dim3(cap / 128, n_kv_heads * rep), bwd::dkv2::NTHREADS, bwd::dkv2::SMEM, st>>>(
+      tq128, tdo128, tk, tv, rows, counts, selected, sel_counts, lse2c, Dc, visc, rep, seq_len, cap, capq, dK_sel,
+      dV_sel);
   return omni_launch_check();
 }
 
+#ifdef OMNI_VARIANTS
 // Profiling support (OMNI_BWD_PROBE=3): copies the 8 dkv phase-cycle sums to
 // host memory and resets them.
 extern "C" int omni_debug_bwd_trace(unsigned long long* host8) {
@@ -1116,6 +1132,7 @@ extern "C" int omni_debug_bwd_trace(unsigned long long* host8) {
   OMNI_CUDA_TRY(cudaMemcpyToSymbol(bwd::g_bwd_trace, z, sizeof(z)));
   return OMNI_OK;
 }
+#endif  // OMNI_VARIANTS
 
 extern "C" int omni_sparse_attn_bwd(const void* Q, const void* K_sel, const void* V_sel, const void* O, const void* dO,
                                     const float* lse, const int32_t* rows, const int32_t* counts,

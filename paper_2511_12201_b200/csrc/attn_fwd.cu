@@ -578,10 +578,12 @@ int omni_make_tmap_rows(CUtensorMap* map, const void* base, uint64_t rows, uint6
 
 static constexpr int kDefaultPoly = 6;
 
+#ifdef OMNI_VARIANTS
 int omni_sparse_attn_fwd_pair(const void* Q, const void* K_sel, const void* V_sel, const void* V, const int32_t* rows,
                               const int32_t* counts, const int32_t* selected, const int32_t* sel_counts,
                               int n_q_heads, int n_kv_heads, int seq_len, int cap, int sink_index, void* O,
                               float* lse, int poly, cudaStream_t stream);
+#endif
 
 // status: device int workspace (nullable). With it the FAST kernel runs first
 // and the safe kernel is launched behind it, exiting at once unless a tile's
@@ -597,6 +599,8 @@ extern "C" int omni_sparse_attn_fwd_ex(const void* Q, const void* K_sel, const v
   OMNI_CHECK(cap >= 128 && cap % 128 == 0, OMNI_E_SHAPE, "cap must be a positive multiple of 128");
   OMNI_CHECK(sink_index >= 0 && sink_index < seq_len, OMNI_E_LAYOUT, "sink_index outside the sequence");
   OMNI_CHECK(seq_len >= 1, OMNI_E_SHAPE, "empty sequence");
+  cudaStream_t st_ = static_cast<cudaStream_t>(stream);
+#ifdef OMNI_VARIANTS
   // Kernel choice: the single-CTA two-Q-tile ping-pong kernel below by
   // default (measured fastest at the 64K bench workload); OMNI_FWD_IMPL=pair
   // selects the CTA-pair kernel of attn_fwd2.cu (faster MMA/TMA pipeline, 6.8
@@ -610,7 +614,6 @@ extern "C" int omni_sparse_attn_fwd_ex(const void* Q, const void* K_sel, const v
     const char* e = getenv("OMNI_FWD_POLY");
     return e ? atoi(e) : kDefaultPoly;
   }();
-  cudaStream_t st_ = static_cast<cudaStream_t>(stream);
   if (!single)
     return omni_sparse_attn_fwd_pair(Q, K_sel, V_sel, V, rows, counts, selected, sel_counts, n_q_heads, n_kv_heads,
                                      seq_len, cap, sink_index, O, lse, poly_env, st_);
@@ -655,6 +658,27 @@ extern "C" int omni_sparse_attn_fwd_ex(const void* Q, const void* K_sel, const v
     OMNI_CUDA_TRY(omni_smem_attr(fast, (int)fwd::SMEM_BYTES));
     OMNI_CUDA_TRY(omni_smem_attr(redo, (int)fwd::SMEM_BYTES));
   }
+#else
+  // Product build: the single-CTA two-Q-tile ping-pong kernel with 6 of 16
+  // exponential pairs on the FMA-pipe polynomial, fast (deferred agreement)
+  // with the safe kernel as its fallback. The measured alternatives (CTA
+  // pair, other splits, per-phase tracing) live in the OMNI_VARIANTS build
+  // (libomnisparse_variants.so, profiles/r01_k4_notes.md).
+  CUtensorMap tk, tv;
+  int st = omni_make_tmap_rows(&tk, K_sel, (uint64_t)n_kv_heads * cap, 128, 2, 64, fwd::BN);
+  if (st) return st;
+  st = omni_make_tmap_rows(&tv, V_sel, (uint64_t)n_kv_heads * cap, 128, 2, 64, fwd::BN);
+  if (st) return st;
+  auto safe = fwd::sparse_fwd_kernel<kDefaultPoly>;
+  auto fast = fwd::sparse_fwd_kernel<kDefaultPoly, false, true>;
+  auto redo = fwd::sparse_fwd_kernel<kDefaultPoly, false, false, true>;
+  const bool use_fast = status != nullptr;
+  OMNI_CUDA_TRY(omni_smem_attr(safe, (int)fwd::SMEM_BYTES));
+  if (use_fast) {
+    OMNI_CUDA_TRY(omni_smem_attr(fast, (int)fwd::SMEM_BYTES));
+    OMNI_CUDA_TRY(omni_smem_attr(redo, (int)fwd::SMEM_BYTES));
+  }
+#endif
   const int n_tiles = (seq_len + 2 * fwd::BM - 1) / (2 * fwd::BM);
   dim3 grid(n_tiles * n_q_heads);
   const int rep = n_q_heads / n_kv_heads;
@@ -690,6 +714,7 @@ extern "C" int omni_sparse_attn_fwd(const void* Q, const void* K_sel, const void
                                  seq_len, head_dim, cap, sink_index, O, lse, nullptr, stream);
 }
 
+#ifdef OMNI_VARIANTS
 // Profiling support (OMNI_FWD_TRACE=1): copies the 8 per-phase cycle sums
 // of the traced K4 launches to host memory and resets them.
 extern "C" int omni_debug_fwd_trace(unsigned long long* host8) {
@@ -699,3 +724,4 @@ extern "C" int omni_debug_fwd_trace(unsigned long long* host8) {
   OMNI_CUDA_TRY(cudaMemcpyToSymbol(fwd::g_fwd_trace, z, sizeof(z)));
   return OMNI_OK;
 }
+#endif  // OMNI_VARIANTS

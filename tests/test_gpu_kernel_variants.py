@@ -1,5 +1,5 @@
-"""K4 kernel variants (selected once per process by environment variables)
-against the oracle: the single-CTA ping-pong kernel at several MUFU / FMA-pipe
+"""K4 kernel variants (the OMNI_VARIANTS build, libomnisparse_variants.so,
+selected once per process by environment variables) against the oracle: the single-CTA ping-pong kernel at several MUFU / FMA-pipe
 exp2 splits and the CTA-pair (cta_group::2) kernel. Each variant runs in its
 own subprocess on a GQA workload with ragged N (partial tiles, staircase)."""
 
@@ -75,7 +75,8 @@ for _g in range(K.shape[0]):
                                                  ("single", "6", "1", "ramp"), ("single", "6", "0", "ramp"),
                                                  ("pair", "0", "1", False), ("pair", "4", "1", False)])
 def test_forward_variant_matches_oracle(impl, poly, fast, jump):
-    env = dict(os.environ, OMNI_FWD_IMPL=impl, OMNI_FWD_POLY=poly, OMNI_FWD_FAST=fast)
+    env = dict(os.environ, OMNI_FWD_IMPL=impl, OMNI_FWD_POLY=poly, OMNI_FWD_FAST=fast,
+               OMNI_LIBRARY=os.path.join(ROOT, "paper_2511_12201_b200", "lib", "libomnisparse_variants.so"))
     snippet = RAMP if jump == "ramp" else JUMP if jump else ""
     code = CODE.replace("Q, K, V = round_bf16(Q), round_bf16(K), round_bf16(V)",
                         snippet + "Q, K, V = round_bf16(Q), round_bf16(K), round_bf16(V)")
