@@ -378,13 +378,48 @@ __device__ double reduceat_sum(const F& f, int lo, int n) {
   return __dadd_rn(f(lo), pw_serial(f, lo + 1, n - 1));
 }
 
-// CTA-wide pairwise sum of f(0 .. n): leaves in parallel (path p of the
-// depth-D split tree; a leaf reached early is computed by the path whose
-// remaining bits are zero and kept at slot p), then internal nodes bottom up
-// (node (d, q) at slot q << (D - d), right child at (2q + 1) << (D - d - 1)).
-// buf: 2^pw_depth(n) doubles. Every thread returns the sum.
-template <typename F>
-__device__ double np_pairwise_sum(const F& f, int n, double* buf) {
+// Leaf of the pairwise sum over a block-constant vector v(t) = vals[t / B]:
+// the elements are consumed in increasing t with a running block index, so
+// the additions happen in exactly pw_leaf's order without a division per
+// element.
+__device__ __forceinline__ double pw_leaf_blocks(const double* vals, int B, int nb, int lo, int n) {
+  int J = lo / B, rem = lo - J * B;
+  double cur = vals[J];
+  auto next = [&]() {
+    const double v = cur;
+    if (++rem == B) {
+      rem = 0;
+      if (++J < nb) cur = vals[J];
+    }
+    return v;
+  };
+  if (n < 8) {
+    double r = 0.0;
+    for (int i = 0; i < n; ++i) r = __dadd_rn(r, next());
+    return r;
+  }
+  double r[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) r[j] = next();
+  int i = 8;
+  for (; i < n - (n % 8); i += 8) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], next());
+  }
+  double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                         __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+  for (; i < n; ++i) res = __dadd_rn(res, next());
+  return res;
+}
+
+// CTA-wide pairwise sum of n elements whose leaf sums leaf(lo, m) computes:
+// leaves in parallel (path p of the depth-D split tree; a leaf reached early
+// is computed by the path whose remaining bits are zero and kept at slot p),
+// then internal nodes bottom up (node (d, q) at slot q << (D - d), right child
+// at (2q + 1) << (D - d - 1)). buf: 2^pw_depth(n) doubles. Every thread
+// returns the sum.
+template <typename Leaf>
+__device__ double np_pairwise_sum(const Leaf& leaf, int n, double* buf) {
   const int D = pw_depth(n);
   const int L = 1 << D;
   for (int p = threadIdx.x; p < L; p += blockDim.x) {
@@ -394,7 +429,7 @@ __device__ double np_pairwise_sum(const F& f, int n, double* buf) {
       if ((p >> (D - 1 - d)) & 1) { lo += n2; m -= n2; } else { m = n2; }
       ++d;
     }
-    if ((p & ((1 << (D - d)) - 1)) == 0) buf[p] = pw_leaf(f, lo, m);
+    if ((p & ((1 << (D - d)) - 1)) == 0) buf[p] = leaf(lo, m);
   }
   __syncthreads();
   for (int d = D - 1; d >= 0; --d) {
@@ -419,23 +454,31 @@ __device__ double np_pairwise_sum(const F& f, int n, double* buf) {
 }
 
 // _core_py.kurtosis (kv_select.py:49-53) of the per-token vector v(t) =
-// score(t / B), t < N, in NumPy's order. CTA-wide.
-template <typename S>
-__device__ double kurtosis_np(const S& score, int N, int B, double* buf) {
+// score[t / B], t < N, in NumPy's order: mu = v.mean(), d = v - mu,
+// m2 = mean(d * d), m4 = mean(d * d * d * d) (left to right), m4 / m2^2.
+// d and its powers are per block (the same rounded value for every token of
+// a block), staged in tmp[nb]; the means are pairwise sums over the tokens.
+// CTA-wide; score / tmp in shared or global memory.
+__device__ double kurtosis_np(const double* score, double* tmp, int N, int B, double* buf) {
+  const int nb = (N + B - 1) / B;
   const double n = static_cast<double>(N);
-  auto v = [&](int t) { return score(t / B); };
-  const double mu = __ddiv_rn(np_pairwise_sum(v, N, buf), n);
-  auto d2 = [&](int t) {
-    const double d = __dsub_rn(score(t / B), mu);
-    return __dmul_rn(d, d);
-  };
-  const double m2 = __ddiv_rn(np_pairwise_sum(d2, N, buf), n);
-  if (m2 == 0.0) return 0.0;
-  auto d4 = [&](int t) {
-    const double d = __dsub_rn(score(t / B), mu);
-    return __dmul_rn(__dmul_rn(__dmul_rn(d, d), d), d);
-  };
-  const double m4 = __ddiv_rn(np_pairwise_sum(d4, N, buf), n);
+  const double mu = __ddiv_rn(np_pairwise_sum([&](int lo, int m) { return pw_leaf_blocks(score, B, nb, lo, m); },
+                                              N, buf), n);
+  for (int J = threadIdx.x; J < nb; J += blockDim.x) {
+    const double d = __dsub_rn(score[J], mu);
+    tmp[J] = __dmul_rn(d, d);
+  }
+  __syncthreads();
+  const double m2 = __ddiv_rn(np_pairwise_sum([&](int lo, int m) { return pw_leaf_blocks(tmp, B, nb, lo, m); },
+                                              N, buf), n);
+  if (m2 == 0.0) return 0.0;  // uniform across the CTA (every thread holds the same m2)
+  for (int J = threadIdx.x; J < nb; J += blockDim.x) {
+    const double d = __dsub_rn(score[J], mu);
+    tmp[J] = __dmul_rn(__dmul_rn(__dmul_rn(d, d), d), d);
+  }
+  __syncthreads();
+  const double m4 = __ddiv_rn(np_pairwise_sum([&](int lo, int m) { return pw_leaf_blocks(tmp, B, nb, lo, m); },
+                                              N, buf), n);
   return __ddiv_rn(m4, __dmul_rn(m2, m2));
 }
 
@@ -578,7 +621,7 @@ __global__ void __launch_bounds__(1024) select_cluster_kernel(const double* __re
     gscores[(size_t)g * nb + J] = sc;
   }
   __syncthreads();
-  const double kurt = kurtosis_np([&](int J) { return S.score[J]; }, N, B, S.pw);
+  const double kurt = kurtosis_np(S.score, S.pre, N, B, S.pw);
   if (threadIdx.x == 0) S.kurt = kurt;
   // descending token-score order of this group (ties to the lower block)
   for (int J = threadIdx.x; J < nb; J += blockDim.x) S.pre[J] = -S.score[J];
@@ -692,6 +735,7 @@ struct SelWs {
   int* idx_tok;      // [Hkv, stride] block ids, permuted with the keys
   double* key_blk;   // [Hkv, stride] -reduceat block sum
   int* idx_blk;
+  double* tmp;       // [Hkv, nb] kurtosis scratch
   int* take;         // [Hkv, nb] keys taken per block id
   int* rpre;         // [Hkv, nb] scan scratch
   double* pre;       // [nb]
@@ -805,8 +849,7 @@ __global__ void __launch_bounds__(1024) sel_scores_kernel(const double* __restri
     }
   }
   __syncthreads();
-  const double* gs = gscores + (size_t)g * nb;
-  const double kurt = kurtosis_np([gs](int J) { return gs[J]; }, N, B, pwbuf);
+  const double kurt = kurtosis_np(gscores + (size_t)g * nb, ws.tmp + (size_t)g * nb, N, B, pwbuf);
   if (threadIdx.x == 0) stats[g] = kurt;
 }
 
@@ -1042,6 +1085,7 @@ static SelWs sel_layout(void* base, int n_kv_heads, int nb, size_t* total) {
   w.idx_tok = reinterpret_cast<int*>(take(hs * 4));
   w.key_blk = reinterpret_cast<double*>(take(hs * 8));
   w.idx_blk = reinterpret_cast<int*>(take(hs * 4));
+  w.tmp = reinterpret_cast<double*>(take(hn * 8));
   w.take = reinterpret_cast<int*>(take(hn * 4));
   w.rpre = reinterpret_cast<int*>(take(hn * 4));
   w.pre = reinterpret_cast<double*>(take((size_t)nb * 8));
