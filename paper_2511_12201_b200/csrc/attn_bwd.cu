@@ -215,6 +215,9 @@ dq_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
         tma_load_2d(sb + OFF_V + s * TILE, &tm_v, B(B_VF + s), 0, kr0 + j * 128);
         tma_load_2d(sb + OFF_V + s * TILE + ATOM, &tm_v, B(B_VF + s), 64, kr0 + j * 128);
       }
+      // observe the last ring phases (every mbarrier phase is waited on)
+      for (int j = nt > NSK ? nt - NSK : 0; j < nt; ++j) mbar_wait(B(B_KE + j % NSK), (j / NSK) & 1);
+      for (int j = nt > 2 ? nt - 2 : 0; j < nt; ++j) mbar_wait(B(B_VE + (j & 1)), (j >> 1) & 1);
     }
   } else if (warp == 1) {
     // whole warp runs the schedule; elect.sync picks the issuing lane
@@ -762,6 +765,11 @@ dkv2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
         tma_load_2d(sb + OFF_DO + s * TILE, &tm_do, B(B_DF + s), 0, row);
         tma_load_2d(sb + OFF_DO + s * TILE + ATOM, &tm_do, B(B_DF + s), 64, row);
       }
+      // observe the last ring phases (every mbarrier phase is waited on)
+      for (int k = total > 2 ? total - 2 : 0; k < total; ++k) {
+        mbar_wait(B(B_QE + (k & 1)), (k >> 1) & 1);
+        mbar_wait(B(B_DE + (k & 1)), (k >> 1) & 1);
+      }
     }
   } else if (warp == 1) {
     // whole warp runs the schedule; elect.sync picks the issuing lane
@@ -939,6 +947,8 @@ dkv2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
       // phase 2: dS^T = P^T (dP^T - D) with the bf16 P^T (the values dV uses)
       const uint32_t cs0 = clock();
       mbar_wait(B(B_SF), k & 1);
+      // observe the dV / dK(k-1) phase (complete: dP^T(k) was issued after it)
+      if (k > 0) mbar_wait(B(B_PE), (k - 1) & 1);
       const uint32_t cs1 = clock();
       tc_fence_after();
       uint32_t dp[32];

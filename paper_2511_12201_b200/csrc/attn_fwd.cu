@@ -197,6 +197,12 @@ __device__ __forceinline__ void fwd_tile(int L, bool reuse, const CUtensorMap& t
         tma_load_2d(sbase + OFF_V + s * TILE, &tm_v, B(B_VF + s), 0, kr0 + j * BN);
         tma_load_2d(sbase + OFF_V + s * TILE + ATOM, &tm_v, B(B_VF + s), 64, kr0 + j * BN);
       }
+      // observe the last "stage free" phases too (each K / V tile's stage is
+      // committed once; every mbarrier phase is waited on)
+      for (int j = ntm > NST ? ntm - NST : 0; j < ntm; ++j) {
+        mbar_wait(B(B_KE + j % NST), (j / NST) & 1);
+        mbar_wait(B(B_VE + j % NST), (j / NST) & 1);
+      }
     }
   } else if (warp == 1) {
     // ------------------------------------------------------ MMA issuer
@@ -295,6 +301,9 @@ __device__ __forceinline__ void fwd_tile(int L, bool reuse, const CUtensorMap& t
       for (int j = 0; j < nt; ++j) {
         tick(4);
         mbar_wait(B(B_SF + x), j & 1);  // S_X(j) ready (and, in order, PV_X(j-1) done)
+        // observe PV_X(j-1)'s phase (complete already: the commit of S_X(j)
+        // covers every earlier MMA), so every phase of B_PV is waited on
+        if (j > 0) mbar_wait(B(B_PV + x), (j - 1) & 1);
         tc_fence_after();
         tick(0);
         if constexpr (POLY < 0) {  // profiling only: the MMA / TMA pipeline without softmax work
