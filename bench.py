@@ -326,6 +326,20 @@ def decode_section(args, steps, warmup, hbm_peak, tau=None, p=None, dense=True, 
     full_bytes = B * HKV * (n + n_ans0 + steps / 2) * 2 * D * 2
     q_bytes = B * HQ * D * (2 + 4)
     fetched = float(torch.stack([f.view(B, HKV, -1).any(dim=2) for f in flags_log]).float().mean())
+    # The reference's own accounting (FetchLog, decode.py:180-190, and
+    # kv_reduction, metrics.py:94-120): every Q head meters its own fetch —
+    # b vision rows when active, text + answer always — against its own full
+    # cache. Physically (above) a GQA group's vision rows are read once when
+    # ANY of its 7 Q heads is active, so the two differ at rep > 1.
+    act_q = torch.stack([f.view(B, HQ) for f in flags_log]).float().cpu()  # [steps, B, HQ]
+    bud = torch.tensor([float(b) for b in cache.budgets])
+    row = 2 * D * 2
+    ref_fetched = ref_full = 0.0
+    for i in range(act_q.shape[0]):
+        ta = N_TEXT + n_ans0 + i
+        ref_fetched += float((act_q[i] * bud[:, None]).sum() + B * HQ * ta) * row
+        ref_full += B * HQ * (nv + ta) * row
+    ref_vis_frac = float((act_q.sum(dim=(0, 2)) * bud).sum() / (act_q.shape[0] * HQ * nv * B))
     budgets = sum(cache.budgets)
     if world > 1:  # max time over ranks, bytes summed over ranks
         import torch.distributed as dist
@@ -343,6 +357,14 @@ def decode_section(args, steps, warmup, hbm_peak, tau=None, p=None, dense=True, 
         "kv_bytes_reduction": full_bytes / slim_bytes,
         "budgets_mean": budgets / B_all,
         "fetched_group_frac": fetched,
+        "reference_accounting": {
+            "kv_bytes_reduction_per_q_head": ref_full / ref_fetched if ref_fetched else None,
+            "vision_fetch_reduction": 1.0 - ref_vis_frac,
+            "active_q_head_frac": float(act_q.mean()),
+            "note": "the reference's FetchLog / kv_reduction model (each Q head meters b vision rows when active, "
+                    "text+answer always); kv_bytes_reduction above is the physical GQA read (a group's vision rows "
+                    "once if any of its Q heads is active)",
+        },
         "roofline": {"bound": "hbm", "achieved": (slim_bytes + q_bytes) / (ms / 1e3) / 1e9 / world,
                      "peak": hbm_peak, "unit": "GB/s per GPU",
                      "frac": (slim_bytes + q_bytes) / (ms / 1e3) / 1e9 / world / hbm_peak},
@@ -754,6 +776,8 @@ def headline_first(line: dict) -> dict:
         "decode_tok_s": dec.get("tok_s"),
         "decode_kv_bytes_reduction_tau0.08_p0.82": dec.get("kv_bytes_reduction"),
         "decode_kv_bytes_reduction_tau0.12_p0.75": dec2.get("kv_bytes_reduction"),
+        "decode_kv_bytes_reduction_reference_accounting_tau0.08_p0.82":
+            dec.get("reference_accounting", {}).get("kv_bytes_reduction_per_q_head"),
     }
     for k in ("roofline", "parity"):
         if k in line:

@@ -148,8 +148,18 @@ __global__ void probe_finish_kernel(const T* __restrict__ K, int N, int d, int n
   const int col = threadIdx.x & 31, ph = threadIdx.x >> 5;
   const int c = blockIdx.x * 32 + col;
   double s = 0.0;
-  if (c < d)
-    for (int J = ph; J < nb; J += 32) s += vis_part[((size_t)g * nb + J) * d + c];
+  if (c < d) {
+    // eight independent loads in flight, added in ascending J (fixed order)
+    int J = ph;
+    for (; J + 7 * 32 < nb; J += 8 * 32) {
+      double v[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] = vis_part[((size_t)g * nb + J + 32 * k) * d + c];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) s += v[k];
+    }
+    for (; J < nb; J += 32) s += vis_part[((size_t)g * nb + J) * d + c];
+  }
   part[ph][col] = s;
   __syncthreads();
   if (ph == 0 && c < d) {
@@ -440,6 +450,326 @@ __global__ void __launch_bounds__(256, 3) q_score_bulk_kernel(const __nv_bfloat1
   }
 }
 
+// ------------------------------------------------- K1 / K2 persistent streams
+// The hot-path instances (bf16, d = 128, probe blocks of <= 256 rows): one
+// CTA per SM walks the (head, block) items c, c + G, c + 2G, ... and streams
+// each item's rows (<= 64 KB) into a 3-stage shared-memory ring with one
+// cp.async.bulk per item, so two items' reads are always in flight while the
+// third is consumed. The per-item column sums (pooled Q / K, float64) are
+// reduced through a double-buffered shared-memory slab in a fixed order.
+constexpr int SP_STAGES = 3;
+constexpr uint32_t SP_STAGE = 256 * 256;  // one probe block of bf16 rows, d = 128
+
+__device__ __forceinline__ float bf_lo(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf_hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
+
+// Exact bf16 -> float64 on the integer pipes (F2F.F64.F32 issues to the XU
+// pipe, whose conversion rate made it the limiter of K1 / K2: 66 % busy).
+// f = the value's fp32 bits (low 16 bits zero). For a normal number the
+// float64 high word is sign | (exp8 + 896) << 20 | mant7 << 13 and the low
+// word is 0; +-0 keeps just the sign. Denormal / inf / nan bf16 values are
+// flagged (*odd) and converted by the caller with the hardware instruction.
+__device__ __forceinline__ double bf32_to_f64(uint32_t f) {
+  const uint32_t a = f & 0x7FFFFFFFu;
+  const uint32_t hi = a != 0u ? (((a >> 3) + 0x38000000u) | (f & 0x80000000u)) : f;
+  return __hiloint2double(static_cast<int>(hi), 0);
+}
+
+// item -> (head, block) and its row span
+struct SpItem {
+  int h, J, r0, nr;
+};
+__device__ __forceinline__ SpItem sp_item(int i, int nb, int block, int N) {
+  SpItem it;
+  it.h = i / nb;
+  it.J = i - it.h * nb;
+  it.r0 = it.J * block;
+  it.nr = min(N, it.r0 + block) - it.r0;
+  return it;
+}
+__device__ __forceinline__ void sp_issue(const __nv_bfloat16* src, int nb, int block, int N, int i, uint32_t dst,
+                                         uint32_t bar) {
+  const SpItem it = sp_item(i, nb, block, N);
+  const uint32_t bytes = (uint32_t)it.nr * 256u;
+  mbar_expect_tx(bar, bytes);
+  bulk_g2s(dst, reinterpret_cast<const uint8_t*>(src + ((size_t)it.h * N + it.r0) * 128), bytes, bar);
+}
+
+// K2: the decision needs only the sign of l1 - l0 - T with l1 - l0 = q . kd,
+// kd = (k_act - k_lazy) / sqrt(d): one fp32 dot product (FFMA2 pairs) per row
+// instead of two float64 ones, with a rigorous error bound. kd is rounded to
+// fp32 once (relative error u = 2^-24 per component), q is exact in fp32, and
+// every partial sum is a chain of at most 8 roundings (the pair FMA, the pair
+// add, 5 cross-lane adds), so
+//   |d32 - q . kd| <= 9 u sum_i |q_i kd_i| <= 9 u ||q||_2 ||kd||_2
+// (Cauchy-Schwarz; ||q||^2 is accumulated alongside in fp32 and the bound
+// taken as 13 u and inflated by 1 %). Rows with |d32 - T| beyond that bound
+// plus q_score_bulk_kernel's own 1e-9 band get the decision
+// q_score_bulk_kernel's float64 path takes (its l1 - l0 differs from q . kd
+// by far less than the band); the rest (a few rows per million) are
+// re-evaluated from shared memory with q_score_bulk_kernel's float64
+// arithmetic, operation for operation.
+//
+// Layout: lane L owns columns 4L..4L+3 (one 8-byte load per row: a warp reads
+// a whole 256-byte row, conflict-free) and a warp owns 16 rows of the item.
+// The 16 per-row partials are reduce-scattered over the lanes (xor 16, 8, 4,
+// 2, then a butterfly on xor 1) without selects: register slot k of lane L
+// holds row k ^ m(L), m(L) = the lane bits 4..1 reversed into 8/4/2/1, so at
+// every level each lane keeps its low slots and sends its high ones, and
+// lanes 2j, 2j + 1 end with row m(2j). Pooled Q column sums (float64) need no
+// cross-lane work: each lane owns its columns.
+#ifndef OMNI_QP_WARPS
+#define OMNI_QP_WARPS 16
+#endif
+constexpr int QP_WARPS = OMNI_QP_WARPS;
+constexpr int QP_ROWS = 256 / QP_WARPS;  // rows per warp and item
+constexpr int QP_LEVELS = QP_ROWS == 16 ? 4 : QP_ROWS == 8 ? 3 : 2;
+constexpr int QP_SHARE = 32 / QP_ROWS;   // lanes that end with the same row
+constexpr int QP_SLABS = QP_WARPS <= 16 ? 2 : 1;  // double-buffered column-sum slab when it fits
+constexpr uint32_t QP_SMEM = SP_STAGES * SP_STAGE + QP_SLABS * QP_WARPS * 128 * 8;
+
+// slot k of lane L holds row k ^ m(L): lane bits 4, 3, ... reversed
+__device__ __forceinline__ int sp_row_mask(int lane) {
+  int m = 0;
+#pragma unroll
+  for (int l = 0; l < QP_LEVELS; ++l) m |= ((lane >> (4 - l)) & 1) << (QP_LEVELS - 1 - l);
+  return m;
+}
+
+__global__ void __launch_bounds__(QP_WARPS * 32, 1) q_score_stream_kernel(
+    const __nv_bfloat16* __restrict__ Q, int N, int nb, int n_items, int rep, int n_vision, double tau,
+    double tau_logit, int preserve, int block, const double* __restrict__ k_lazy, const double* __restrict__ k_act,
+    uint8_t* __restrict__ active, double* __restrict__ pooled_q, int32_t* __restrict__ block_active,
+    __nv_bfloat16* __restrict__ o_zero) {
+  constexpr int d = 128;
+  extern __shared__ __align__(1024) uint8_t sp_smem[];
+  __shared__ __align__(8) uint64_t bars[SP_STAGES];
+  __shared__ int s_cnt[QP_SLABS][QP_WARPS];
+  double* s_pool = reinterpret_cast<double*>(sp_smem + SP_STAGES * SP_STAGE);  // [slabs][warps][128]
+  const uint32_t ring = smem_u32(sp_smem);
+  const int G = gridDim.x;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < SP_STAGES; ++s) mbar_init(smem_u32(&bars[s]), 1);
+    fence_mbar_init();
+    for (int k = 0; k < SP_STAGES; ++k) {
+      const int i = blockIdx.x + k * G;
+      if (i < n_items) sp_issue(Q, nb, block, N, i, ring + k * SP_STAGE, smem_u32(&bars[k]));
+    }
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m = sp_row_mask(lane);
+  const double scale = 1.0 / sqrt(static_cast<double>(d));
+  const double band = 1e-9 * (1.0 + fabs(tau_logit));
+  uint64_t kd01 = 0, kd23 = 0;
+  double kbound = 0.0;
+  float kboundf = 0.f;
+  int cur_g = -1;
+  for (int k = 0;; ++k) {
+    const int i = blockIdx.x + k * G;
+    if (i >= n_items) break;
+    const int s = k % SP_STAGES;
+    const SpItem it = sp_item(i, nb, block, N);
+    const int h = it.h, g = h / rep, r0 = it.r0, nr = it.nr;
+    if (g != cur_g) {  // kd of this lane's 4 columns; ||kd||_2 over the warp
+      cur_g = g;
+      double v[4], kdn2 = 0.0;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const size_t o = (size_t)g * d + 4 * lane + e;
+        v[e] = (__ldg(k_act + o) - __ldg(k_lazy + o)) * scale;
+        kdn2 = fma(v[e], v[e], kdn2);
+      }
+      kd01 = f32x2(static_cast<float>(v[0]), static_cast<float>(v[1]));
+      kd23 = f32x2(static_cast<float>(v[2]), static_cast<float>(v[3]));
+      kdn2 = warp_sum(kdn2);
+      kbound = 13.0 * 0x1p-24 * sqrt(kdn2) * 1.02;  // 13 u ||kd||, inflated for fp32 ||q||^2 and sqrtf
+      kboundf = static_cast<float>(kbound) * 1.0001f;
+    }
+    const uint8_t* qsm = sp_smem + s * SP_STAGE;
+    double pool[4] = {0.0, 0.0, 0.0, 0.0};
+    int cnt = 0;
+    mbar_wait(smem_u32(&bars[s]), (k / SP_STAGES) & 1);
+    const int rbase = warp * QP_ROWS;
+    if (rbase < nr) {
+      float dv[QP_ROWS], nv[QP_ROWS];
+#pragma unroll
+      for (int kk = 0; kk < QP_ROWS; ++kk) {
+        const int rr = rbase + (kk ^ m);
+        uint2 w = make_uint2(0u, 0u);
+        if (rr < nr) w = *reinterpret_cast<const uint2*>(qsm + (size_t)rr * (d * 2) + lane * 8);
+        const float a0 = bf_lo(w.x), a1 = bf_hi(w.x), a2 = bf_lo(w.y), a3 = bf_hi(w.y);
+        const uint64_t x01 = f32x2(a0, a1), x23 = f32x2(a2, a3);
+        const uint64_t acc = ffma2(x23, kd23, ffma2(x01, kd01, f32x2(0.f, 0.f)));
+        const uint64_t nrm = ffma2(x23, x23, ffma2(x01, x01, f32x2(0.f, 0.f)));
+        dv[kk] = f32x2_lo(acc) + f32x2_hi(acc);
+        nv[kk] = f32x2_lo(nrm) + f32x2_hi(nrm);
+        pool[0] += static_cast<double>(a0);
+        pool[1] += static_cast<double>(a1);
+        pool[2] += static_cast<double>(a2);
+        pool[3] += static_cast<double>(a3);
+      }
+      // reduce-scatter: keep the low half of the slots, send the high half
+#pragma unroll
+      for (int half = QP_ROWS / 2, msk = 16; half >= 1; half >>= 1, msk >>= 1) {
+#pragma unroll
+        for (int kk = 0; kk < half; ++kk) {
+          dv[kk] += __shfl_xor_sync(0xffffffffu, dv[kk + half], msk);
+          nv[kk] += __shfl_xor_sync(0xffffffffu, nv[kk + half], msk);
+        }
+      }
+#pragma unroll
+      for (int msk = QP_SHARE / 2; msk >= 1; msk >>= 1) {
+        dv[0] += __shfl_xor_sync(0xffffffffu, dv[0], msk);
+        nv[0] += __shfl_xor_sync(0xffffffffu, nv[0], msk);
+      }
+      // the QP_SHARE lanes of row m decide it identically
+      const int rr = rbase + m, r = r0 + rr;
+      const bool mine = rr < nr;
+      int act = 1;
+      bool near = false;
+      if (mine && r < n_vision && !(preserve && h == 0)) {
+        const double dd = static_cast<double>(dv[0]);
+        if (fabs(dd - tau_logit) > static_cast<double>(kboundf * sqrtf(nv[0])) + band) act = dd > tau_logit ? 1 : 0;
+        else near = (lane & (QP_SHARE - 1)) == 0;
+      }
+      unsigned nearm = __ballot_sync(0xffffffffu, near);
+      while (nearm) {
+        // rare: q_score_bulk_kernel's float64 evaluation, operation for
+        // operation (16 lanes x 8 columns, FMA chains in column order, the
+        // xor 8 / 4 / 2 / 1 tree), so verdict and p agree with the want_prob path
+        const int fl = __ffs(nearm) - 1;
+        nearm &= nearm - 1;
+        const int ru = rbase + sp_row_mask(fl);
+        const int cl = lane & 15;
+        const uint4 q = *reinterpret_cast<const uint4*>(qsm + (size_t)ru * (d * 2) + cl * 16);
+        const __nv_bfloat16* hv = reinterpret_cast<const __nv_bfloat16*>(&q);
+        double sl = 0.0, sa = 0.0;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const double v = static_cast<double>(__bfloat162float(hv[e]));
+          sl = fma(v, __ldg(k_lazy + (size_t)g * d + cl * 8 + e), sl);
+          sa = fma(v, __ldg(k_act + (size_t)g * d + cl * 8 + e), sa);
+        }
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) {
+          sl += __shfl_xor_sync(0xffffffffu, sl, o);
+          sa += __shfl_xor_sync(0xffffffffu, sa, o);
+        }
+        const int a = two_way_active(sl * scale, sa * scale, tau, tau_logit, nullptr);
+        if ((lane / QP_SHARE) == (fl / QP_SHARE)) act = a;
+      }
+      if (mine && (lane & (QP_SHARE - 1)) == 0) {
+        active[(size_t)h * N + r] = static_cast<uint8_t>(act);
+        cnt += act;
+      }
+      // a lazy row's output row is zeroed by its QP_SHARE lanes
+      if (o_zero && mine && !act) {
+        constexpr int per = 16 / QP_SHARE;  // 16-byte stores per lane
+        uint4* orow = reinterpret_cast<uint4*>(o_zero + ((size_t)h * N + r) * d) + (lane & (QP_SHARE - 1)) * per;
+#pragma unroll
+        for (int c = 0; c < per; ++c) orow[c] = make_uint4(0, 0, 0, 0);
+      }
+    }
+    const int sl = QP_SLABS == 2 ? (k & 1) : 0;
+    double* slab = s_pool + (size_t)sl * QP_WARPS * d;
+    *reinterpret_cast<double2*>(slab + warp * d + 4 * lane) = make_double2(pool[0], pool[1]);
+    *reinterpret_cast<double2*>(slab + warp * d + 4 * lane + 2) = make_double2(pool[2], pool[3]);
+    cnt = warp_sum(cnt);
+    if (lane == 0) s_cnt[sl][warp] = cnt;
+    __syncthreads();  // stage s consumed, slab complete
+    if (threadIdx.x == 0 && i + SP_STAGES * G < n_items)
+      sp_issue(Q, nb, block, N, i + SP_STAGES * G, ring + s * SP_STAGE, smem_u32(&bars[s]));
+    if (threadIdx.x < d) {
+      double t = 0.0;
+#pragma unroll
+      for (int w = 0; w < QP_WARPS; ++w) t += slab[w * d + threadIdx.x];
+      pooled_q[((size_t)h * nb + it.J) * d + threadIdx.x] = t / static_cast<double>(nr);
+    } else if (threadIdx.x == d) {
+      int t = 0;
+      for (int w = 0; w < QP_WARPS; ++w) t += s_cnt[sl][w];
+      block_active[(size_t)h * nb + it.J] = t;
+    }
+    if (QP_SLABS == 1) __syncthreads();  // slab and counts read before the next item writes them
+  }
+}
+
+// K1: pooled K (all rows) and the vision partial (rows < n_vision, summed
+// separately only on blocks that reach past the vision span) per block,
+// float64. Lane L owns columns 4L..4L+3 (8-byte loads, a warp reads whole
+// rows) and a warp owns 32 rows of the item: no cross-lane reduction.
+constexpr int KP_WARPS = 8;
+constexpr uint32_t KP_SMEM = SP_STAGES * SP_STAGE + 2 * 2 * KP_WARPS * 128 * 8;
+
+__global__ void __launch_bounds__(KP_WARPS * 32, 1) kv_probe_stream_kernel(const __nv_bfloat16* __restrict__ K, int N,
+                                                                           int nb, int n_items, int n_vision, int block,
+                                                                           double* __restrict__ pooled_k,
+                                                                           double* __restrict__ vis_part) {
+  constexpr int d = 128;
+  extern __shared__ __align__(1024) uint8_t sp_smem[];
+  __shared__ __align__(8) uint64_t bars[SP_STAGES];
+  double* s_red = reinterpret_cast<double*>(sp_smem + SP_STAGES * SP_STAGE);  // [2][all|vis][warps][128]
+  const uint32_t ring = smem_u32(sp_smem);
+  const int G = gridDim.x;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < SP_STAGES; ++s) mbar_init(smem_u32(&bars[s]), 1);
+    fence_mbar_init();
+    for (int k = 0; k < SP_STAGES; ++k) {
+      const int i = blockIdx.x + k * G;
+      if (i < n_items) sp_issue(K, nb, block, N, i, ring + k * SP_STAGE, smem_u32(&bars[k]));
+    }
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int k = 0;; ++k) {
+    const int i = blockIdx.x + k * G;
+    if (i >= n_items) break;
+    const int s = k % SP_STAGES;
+    const SpItem it = sp_item(i, nb, block, N);
+    const bool split = it.r0 + it.nr > n_vision;
+    const uint8_t* ksm = sp_smem + s * SP_STAGE;
+    double all[4] = {0.0, 0.0, 0.0, 0.0}, vis[4] = {0.0, 0.0, 0.0, 0.0};
+    mbar_wait(smem_u32(&bars[s]), (k / SP_STAGES) & 1);
+    const int rend = min(it.nr, (warp + 1) * 32);
+#pragma unroll 8
+    for (int rr = warp * 32; rr < rend; ++rr) {
+      const uint2 w = *reinterpret_cast<const uint2*>(ksm + (size_t)rr * (d * 2) + lane * 8);
+      const double a0 = bf_lo(w.x), a1 = bf_hi(w.x), a2 = bf_lo(w.y), a3 = bf_hi(w.y);
+      all[0] += a0;
+      all[1] += a1;
+      all[2] += a2;
+      all[3] += a3;
+      if (split && it.r0 + rr < n_vision) {
+        vis[0] += a0;
+        vis[1] += a1;
+        vis[2] += a2;
+        vis[3] += a3;
+      }
+    }
+    double* slab = s_red + (size_t)(k & 1) * 2 * KP_WARPS * d;
+    *reinterpret_cast<double2*>(slab + warp * d + 4 * lane) = make_double2(all[0], all[1]);
+    *reinterpret_cast<double2*>(slab + warp * d + 4 * lane + 2) = make_double2(all[2], all[3]);
+    if (split) {
+      *reinterpret_cast<double2*>(slab + (KP_WARPS + warp) * d + 4 * lane) = make_double2(vis[0], vis[1]);
+      *reinterpret_cast<double2*>(slab + (KP_WARPS + warp) * d + 4 * lane + 2) = make_double2(vis[2], vis[3]);
+    }
+    __syncthreads();  // stage s consumed, slab complete
+    if (threadIdx.x == 0 && i + SP_STAGES * G < n_items)
+      sp_issue(K, nb, block, N, i + SP_STAGES * G, ring + s * SP_STAGE, smem_u32(&bars[s]));
+    if (threadIdx.x < d) {
+      double a = 0.0, v = 0.0;
+#pragma unroll
+      for (int w = 0; w < KP_WARPS; ++w) {
+        a += slab[w * d + threadIdx.x];
+        if (split) v += slab[(KP_WARPS + w) * d + threadIdx.x];
+      }
+      const size_t o = ((size_t)it.h * nb + it.J) * d + threadIdx.x;
+      pooled_k[o] = a / static_cast<double>(it.nr);
+      vis_part[o] = split ? v : a;
+    }
+  }
+}
+
 // ------------------------------------------------------------- compaction
 // CTA (block J, head h): offset = active rows in earlier blocks, then a
 // block-wide exclusive scan of this block's flags.
@@ -549,6 +879,22 @@ using namespace omni;
 
 static inline int nblocks(int n, int b) { return (n + b - 1) / b; }
 
+// OMNI_QSCORE_F64=1 (tests / A-B): the float64 q_score_bulk_kernel for every
+// row instead of the fp32-with-bound fast kernel.
+static int num_sms() {
+  int dev = 0, n = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n;
+}
+
+static bool fast_off() {
+  static const bool off = [] {
+    const char* e = getenv("OMNI_QSCORE_F64");
+    return e && atoi(e) != 0;
+  }();
+  return off;
+}
+
 extern "C" size_t omni_kv_probe_workspace(int n_kv_heads, int seq_len, int head_dim, int block_size) {
   if (block_size < 1) return 0;
   return sizeof(double) * (size_t)n_kv_heads * nblocks(seq_len, block_size) * head_dim;
@@ -570,7 +916,14 @@ extern "C" int omni_kv_probe(const void* K, int dtype, int n_kv_heads, int seq_l
   const size_t shm = sizeof(double) * 2 * lanes * head_dim;
   dim3 grid(nb, n_kv_heads);
   double* vis = static_cast<double*>(workspace);
-  if (dtype == OMNI_DTYPE_BF16) {
+  if (dtype == OMNI_DTYPE_BF16 && head_dim == 128 && block_size <= QSB_MAX_ROWS) {
+    const int items = nb * n_kv_heads;
+    OMNI_CUDA_TRY(omni_smem_attr(kv_probe_stream_kernel, (int)KP_SMEM));
+    kv_probe_stream_kernel<<<std::min(items, num_sms()), KP_WARPS * 32, KP_SMEM, s>>>(
+        static_cast<const __nv_bfloat16*>(K), seq_len, nb, items, n_vision, block_size, pooled_k, vis);
+    probe_finish_kernel<__nv_bfloat16><<<dim3(4, n_kv_heads), 1024, 0, s>>>(
+        static_cast<const __nv_bfloat16*>(K), seq_len, head_dim, nb, n_vision, sink_index, vis, k_lazy, k_act);
+  } else if (dtype == OMNI_DTYPE_BF16) {
     kv_probe_kernel<__nv_bfloat16><<<grid, 256, shm, s>>>(static_cast<const __nv_bfloat16*>(K), seq_len, head_dim,
                                                             n_vision, block_size, pooled_k, vis);
     probe_finish_kernel<__nv_bfloat16><<<dim3((head_dim + 31) / 32, n_kv_heads), 1024, 0, s>>>(static_cast<const __nv_bfloat16*>(K), seq_len,
@@ -608,7 +961,14 @@ extern "C" int omni_q_score(const void* Q, int dtype, int n_q_heads, int n_kv_he
   const int rep = n_q_heads / n_kv_heads;
   const double T = tau > 0.0 ? log(tau / (1.0 - tau)) : -INFINITY;  // decision threshold on l1 - l0
   __nv_bfloat16* oz = static_cast<__nv_bfloat16*>(O_zero);
-  if (dtype == OMNI_DTYPE_BF16 && head_dim == 128 && block_size >= 64 && block_size <= QSB_MAX_ROWS) {
+  if (dtype == OMNI_DTYPE_BF16 && head_dim == 128 && block_size >= 64 && block_size <= QSB_MAX_ROWS &&
+      p_act == nullptr && tau > 0.0 && !fast_off()) {
+    const int items = (int)grid.x * n_q_heads;
+    OMNI_CUDA_TRY(omni_smem_attr(q_score_stream_kernel, (int)QP_SMEM));
+    q_score_stream_kernel<<<std::min(items, num_sms()), QP_WARPS * 32, QP_SMEM, s>>>(
+        static_cast<const __nv_bfloat16*>(Q), seq_len, (int)grid.x, items, rep, n_vision, tau, T, preserve_first_head,
+        block_size, k_lazy, k_act, active, pooled_q, block_active, oz);
+  } else if (dtype == OMNI_DTYPE_BF16 && head_dim == 128 && block_size >= 64 && block_size <= QSB_MAX_ROWS) {
     const int shm = block_size * head_dim * 2;
     OMNI_CUDA_TRY(omni_smem_attr(q_score_bulk_kernel, QSB_MAX_ROWS * 128 * 2));  // one limit for every block size
     q_score_bulk_kernel<<<grid, 256, shm, s>>>(static_cast<const __nv_bfloat16*>(Q), seq_len, rep, n_vision, tau, T,

@@ -258,3 +258,35 @@ def test_q_score_decision_at_the_boundary(dtype):
         # rows in the ambiguous band: the GPU's verdict is its own p > tau
         np.testing.assert_array_equal(got[~clear], p[~clear] > tau)
         assert int((~clear).sum()) <= 4
+
+
+@pytest.mark.parametrize("seed", [0, 5])
+def test_q_score_fast_kernel_equals_float64_verdicts(seed):
+    """The hot-path K2 (fp32 dot product with a rigorous error bound, float64
+    re-evaluation inside it) gives exactly the verdicts p_act > tau of the
+    float64 kernel (want_prob path, query_select.py:63-68) on every row —
+    including taus placed ON rows' p (exact ties: the bound must route them to
+    the float64 evaluation) and the lazy-row zeroing of O."""
+    from paper_2511_12201_b200 import ops
+    from paper_2511_12201_b200.synthetic import generate_device
+
+    n, nv = 16384, 16384 - 64
+    Q, K, _ = generate_device(28, 4, 128, nv, 64, seed=seed, lazy_fraction=0.5)
+    kl, ka, pk = ops.kv_probe(K, nv, 0, 256)
+    _, p, pooled_ref, bact_ref = ops.q_score(Q, kl, ka, nv, 0.08, True, 256, want_prob=True)
+    pc = p.cpu().numpy()
+    taus = [0.08, 0.5, float(pc[3, 100]), float(pc[17, 9000]), float(pc[27, nv - 1])]
+    for tau in taus:
+        if not 0.0 < tau < 1.0:
+            continue
+        O = torch.full_like(Q, 1.0)
+        act, _, pooled, bact = ops.q_score(Q, kl, ka, nv, tau, True, 256, O_zero=O)
+        got = act.cpu().numpy().astype(bool)
+        exp = np.ones_like(got)
+        exp[:, :nv] = pc > tau
+        exp[0, :] = True  # preserve_first_head
+        np.testing.assert_array_equal(got, exp)
+        assert torch.equal(pooled, pooled_ref) or torch.allclose(pooled, pooled_ref, rtol=1e-13, atol=1e-15)
+        assert torch.equal(bact.sum(dim=1), act.sum(dim=1, dtype=torch.int32))
+        lazy = ~act.bool()
+        assert bool((O[lazy] == 0).all()) and bool((O[~lazy] == 1).all())
