@@ -577,6 +577,357 @@ sparse_fwd_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constan
                               sel_stride, sink, n_tiles_max, O, lse, status);
 }
 
+#ifdef OMNI_VARIANTS
+// ---------------------------------------------------------------------------
+// Row-per-thread variant (OMNI_FWD_IMPL=rpt): 8 softmax warps, 4 per Q tile,
+// each thread owns one full row of S / P / O (128 key columns), so the row
+// maximum, sum and the lazy-rescale decision need no exchange or named
+// barrier between threads. Same TMA / MMA schedule as fwd_tile; P of a key
+// tile is stored packed over the first 64 columns of the tile's S region
+// (K-step kk of PV reads columns 8kk..8kk+7). Fast path: exponentials
+// against the running max, growth settled from the row sum afterwards (as in
+// fwd_tile's FAST mode, a jump beyond 2^64 flags *status for the redo
+// launch); a warp whose rows see their first visible keys takes the two-pass
+// path (row max, then exponentials).
+namespace rpt {
+constexpr int NTHREADS = 320;
+}
+
+template <int POLY>
+__device__ __forceinline__ void fwd_tile_rpt(int L, const CUtensorMap& tm_k, const CUtensorMap& tm_v,
+                                             const __nv_bfloat16* __restrict__ Q,
+                                             const __nv_bfloat16* __restrict__ Vorig,
+                                             const int32_t* __restrict__ rows, const int32_t* __restrict__ counts,
+                                             const int32_t* __restrict__ sel, const int32_t* __restrict__ sel_counts,
+                                             int Hq, int rep, int N, int cap, int sel_stride, int sink,
+                                             __nv_bfloat16* __restrict__ O, float* __restrict__ lse,
+                                             int* __restrict__ status) {
+  extern __shared__ uint8_t smem_raw[];
+  const int h = L % Hq;
+  int cmax = 0;
+  for (int k = threadIdx.x & 31; k < Hq; k += 32) cmax = max(cmax, __ldg(counts + k));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) cmax = max(cmax, __shfl_xor_sync(0xffffffffu, cmax, o));
+  const int tile = (cmax + 2 * BM - 1) / (2 * BM) - 1 - L / Hq;
+  const int cnt = __ldg(counts + h);
+  const int row0 = tile * 2 * BM;
+  if (tile < 0 || row0 >= cnt) return;
+
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sbase = smem_u32(smem);
+  const uint32_t bar = sbase + OFF_BAR;
+  auto B = [&](int i) { return bar + 8u * i; };
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + OFF_TMEM);
+  __shared__ int s_nt[2];
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = h / rep;
+  const int nsel = __ldg(sel_counts + g);
+  const int32_t* selg = sel + (size_t)g * sel_stride;
+  const int32_t* rows_t = rows + (size_t)h * N + row0;
+
+  const int xs = (warp - 2) >> 2;          // Q tile of a softmax warp
+  const int is = (warp & 3) * 32 + lane;   // its row == TMEM lane
+  const int nrows_s = min(BM, cnt - row0 - xs * BM);
+  const bool rvalid = warp >= 2 && is < nrows_s;
+  const int pos = rvalid ? __ldg(rows_t + xs * BM + is) : 0;
+  uint4 qv[16];
+  if (warp >= 2) {
+    const uint4* qrow = reinterpret_cast<const uint4*>(Q + ((size_t)h * N + pos) * D);
+#pragma unroll
+    for (int c = 0; c < 16; ++c) qv[c] = rvalid ? __ldg(qrow + c) : make_uint4(0, 0, 0, 0);
+  }
+  const int vis = rvalid ? count_le(selg, nsel, pos) : 0;
+  if (warp >= 2) {
+    if (is == nrows_s - 1) s_nt[xs] = (vis + BN - 1) / BN;
+    if (nrows_s <= 0 && is == 0) s_nt[xs] = 0;
+  }
+  if (threadIdx.x == 0) {
+    tma_prefetch_desc(&tm_k);
+    tma_prefetch_desc(&tm_v);
+    for (int x = 0; x < 2; ++x) {
+      mbar_init(B(B_QF + x), BM);
+      mbar_init(B(B_SF + x), 1);
+      mbar_init(B(B_PF + x), BM);
+      mbar_init(B(B_PV + x), 1);
+    }
+    for (int s = 0; s < NST; ++s) {
+      mbar_init(B(B_KF + s), 1);
+      mbar_init(B(B_KE + s), 1);
+      mbar_init(B(B_VF + s), 1);
+      mbar_init(B(B_VE + s), 1);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) {
+    tmem_alloc(smem_u32(tmem_slot), TMEM_COLS);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int ntA = s_nt[0], ntB = s_nt[1];
+  const int ntm = max(ntA, ntB);
+
+  if (warp == 0) {
+    if (lane == 0 && ntm > 0) {
+      const int kr0 = g * cap;
+      for (int j = 0; j < ntm; ++j) {
+        const int s = j % NST;
+        const uint32_t ph = ((j / NST) - 1) & 1;
+        if (j >= NST) mbar_wait(B(B_KE + s), ph);
+        mbar_expect_tx(B(B_KF + s), TILE);
+        tma_load_2d(sbase + OFF_K + s * TILE, &tm_k, B(B_KF + s), 0, kr0 + j * BN);
+        tma_load_2d(sbase + OFF_K + s * TILE + ATOM, &tm_k, B(B_KF + s), 64, kr0 + j * BN);
+        if (j >= NST) mbar_wait(B(B_VE + s), ph);
+        mbar_expect_tx(B(B_VF + s), TILE);
+        tma_load_2d(sbase + OFF_V + s * TILE, &tm_v, B(B_VF + s), 0, kr0 + j * BN);
+        tma_load_2d(sbase + OFF_V + s * TILE + ATOM, &tm_v, B(B_VF + s), 64, kr0 + j * BN);
+      }
+      for (int j = ntm > NST ? ntm - NST : 0; j < ntm; ++j) {
+        mbar_wait(B(B_KE + j % NST), (j / NST) & 1);
+        mbar_wait(B(B_VE + j % NST), (j / NST) & 1);
+      }
+    }
+  } else if (warp == 1) {
+    if (ntm > 0) {
+      constexpr uint32_t idesc_qk = idesc_bf16_f32(BM, BN, 0, 0);
+      constexpr uint32_t idesc_pv = idesc_bf16_f32(BM, D, 0, 1);
+      const int nt[2] = {ntA, ntB};
+      const uint64_t dq0 = sdesc_sw128(sbase + OFF_Q, 16, 1024);
+      const uint64_t dk0 = sdesc_sw128(sbase + OFF_K, 16, 1024);
+      const uint64_t dv0 = sdesc_sw128(sbase + OFF_V, ATOM, 1024);
+      auto qk = [&](int x, int j) {
+        const uint64_t qd = dq0 + ((x * TILE) >> 4), kd = dk0 + (((j % NST) * TILE) >> 4);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t off = ((kk >> 2) * ATOM + (kk & 3) * 32) >> 4;
+          umma_bf16_ws(tmem + col_s(x), qd + off, kd + off, idesc_qk, kk > 0 ? 1u : 0u);
+        }
+        umma_commit_ws(B(B_SF + x));
+      };
+      mbar_wait(B(B_KF), 0);
+      for (int x = 0; x < 2; ++x) {
+        if (nt[x] == 0) continue;
+        mbar_wait(B(B_QF + x), 0);
+        tc_fence_after();
+        qk(x, 0);
+      }
+      umma_commit_ws(B(B_KE + 0));
+      for (int j = 0; j < ntm; ++j) {
+        const int s = j % NST;
+        mbar_wait(B(B_VF + s), (j / NST) & 1);
+        bool kwaited = false;
+        const uint64_t vd = dv0 + ((s * TILE) >> 4);
+        for (int x = 0; x < 2; ++x) {
+          if (j >= nt[x]) continue;
+          mbar_wait(B(B_PF + x), j & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk)
+            umma_bf16_ts_ws(tmem + col_o(x), tmem + col_s(x) + kk * 8, vd + ((kk * 2048) >> 4), idesc_pv,
+                            (j > 0 || kk > 0) ? 1u : 0u);
+          umma_commit_ws(B(B_PV + x));
+          if (j + 1 < nt[x]) {
+            if (!kwaited) {
+              mbar_wait(B(B_KF + (j + 1) % NST), ((j + 1) / NST) & 1);
+              tc_fence_after();
+              kwaited = true;
+            }
+            qk(x, j + 1);
+          }
+        }
+        umma_commit_ws(B(B_VE + s));
+        if (kwaited) umma_commit_ws(B(B_KE + (j + 1) % NST));
+      }
+    }
+  } else {
+    // ------------------------------------------------------ softmax warps
+    const int x = xs, i = is;
+    const int nt = x ? ntB : ntA;
+    const uint32_t tl = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+    float m_run = -INFINITY, l_run = 0.f, pend_alpha = 1.f;
+    if (nt > 0) {
+      uint8_t* q_gen = smem + OFF_Q + x * TILE;
+#pragma unroll
+      for (int c = 0; c < 16; ++c) *reinterpret_cast<uint4*>(q_gen + (c >> 3) * ATOM + swz(i, c & 7)) = qv[c];
+      fence_proxy_async_smem();
+      mbar_arrive(B(B_QF + x));
+      const float sl2 = static_cast<float>(kLog2e / sqrt(static_cast<double>(D)));
+      const Exp2PolyConsts pc = exp2_poly_consts();
+      auto exps = [&](auto full_c, const uint32_t* sr, float nmu, uint32_t* pk) -> float {
+        constexpr bool FULL = decltype(full_c)::value;
+        const uint64_t c2 = f32x2(sl2, sl2), n2 = f32x2(nmu, nmu);
+        uint64_t acc0 = f32x2(0.f, 0.f), acc1 = f32x2(0.f, 0.f);
+#pragma unroll
+        for (int c = 0; c < 32; c += 2) {
+          const uint64_t xx = ffma2(f32x2(__uint_as_float(sr[c]), __uint_as_float(sr[c + 1])), c2, n2);
+          uint64_t pp;
+          if (FULL && use_poly<POLY>(c >> 1)) pp = exp2_poly2_pair(xx, pc);
+          else pp = f32x2(fast_exp2(f32x2_lo(xx)), fast_exp2(f32x2_hi(xx)));
+          if ((c & 2) == 0) acc0 = fadd2(acc0, pp); else acc1 = fadd2(acc1, pp);
+          pk[c >> 1] = pack_bf16x2(f32x2_lo(pp), f32x2_hi(pp));
+        }
+        const uint64_t acc = fadd2(acc0, acc1);
+        return f32x2_lo(acc) + f32x2_hi(acc);
+      };
+      auto load_chunk = [&](int q, int lim, bool full, uint32_t* sr) {
+        __syncwarp();
+        tmem_ld32(tl + col_s(x) + q * 32, sr);
+        tmem_wait_ld();
+        if (!full) {
+#pragma unroll
+          for (int c = 0; c < 32; ++c)
+            if (q * 32 + c >= lim) sr[c] = __float_as_uint(-INFINITY);
+        }
+      };
+      auto rescale_o = [&](float a) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint32_t o[32];
+          __syncwarp();
+          tmem_ld32(tl + col_o(x) + q * 32, o);
+          tmem_wait_ld();
+#pragma unroll
+          for (int c = 0; c < 32; ++c) o[c] = __float_as_uint(__uint_as_float(o[c]) * a);
+          tmem_st32(tl + col_o(x) + q * 32, o);
+        }
+      };
+      for (int j = 0; j < nt; ++j) {
+        mbar_wait(B(B_SF + x), j & 1);
+        if (j > 0) mbar_wait(B(B_PV + x), (j - 1) & 1);
+        tc_fence_after();
+        const int lim = vis - j * BN;
+        const bool full = __all_sync(0xffffffffu, lim >= BN);
+        if (__any_sync(0xffffffffu, pend_alpha != 1.f)) {  // O(j-1) complete
+          rescale_o(pend_alpha);
+          pend_alpha = 1.f;
+        }
+        if (!__any_sync(0xffffffffu, m_run == -INFINITY && lim > 0)) {
+          const float nmu = m_run == -INFINITY ? 0.f : -m_run;
+          float rs = 0.f;
+          // chunk q + 1's TMEM load is in flight while chunk q is exponentiated
+          uint32_t sbuf[2][32];
+          __syncwarp();
+          tmem_ld32(tl + col_s(x), sbuf[0]);
+          tmem_wait_ld();
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            uint32_t* sr = sbuf[q & 1];
+            reg_fence32(sr);
+            if (q < 3) tmem_ld32(tl + col_s(x) + (q + 1) * 32, sbuf[(q + 1) & 1]);
+            if (!full) {
+#pragma unroll
+              for (int c = 0; c < 32; ++c)
+                if (q * 32 + c >= lim) sr[c] = __float_as_uint(-INFINITY);
+            }
+            uint32_t pk[16];
+            rs += full ? exps(std::true_type{}, sr, nmu, pk) : exps(std::false_type{}, sr, nmu, pk);
+            tmem_st16(tl + col_s(x) + q * 16, pk);
+            if (q < 3) tmem_wait_ld();
+          }
+          tmem_wait_st();
+          tc_fence_before();
+          mbar_arrive(B(B_PF + x));
+          if (m_run != -INFINITY && !(rs <= 0x1p64f)) atomicExch(status, 1);
+          if (m_run != -INFINITY && rs > 256.f) {
+            const float m_new = m_run + ceilf(__log2f(rs));
+            const float alpha = pow2_int(m_run - m_new);
+            l_run = (l_run + rs) * alpha;
+            pend_alpha = alpha;
+            m_run = m_new;
+          } else {
+            l_run += rs;
+          }
+          continue;
+        }
+        // two-pass path: the row maximum over the visible keys of this tile first
+        float cm = -INFINITY;
+#pragma unroll 1
+        for (int q = 0; q < 4; ++q) {
+          uint32_t sr[32];
+          load_chunk(q, lim, full, sr);
+#pragma unroll
+          for (int c = 0; c < 32; c += 2) cm = fmax3(cm, __uint_as_float(sr[c]), __uint_as_float(sr[c + 1]));
+        }
+        cm *= sl2;
+        float m_fin = m_run;
+        if (cm != -INFINITY && (m_run == -INFINITY || cm > m_run + 8.f)) m_fin = ceilf(cm);
+        const float alpha = (m_run == -INFINITY || m_fin == -INFINITY) ? 1.f : pow2_int(m_run - m_fin);
+        if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) rescale_o(alpha);  // O(j-1) is stable
+        l_run *= alpha;
+        m_run = m_fin;
+        const float nmu = m_run == -INFINITY ? 0.f : -m_run;
+        float rs = 0.f;
+#pragma unroll 1
+        for (int q = 0; q < 4; ++q) {
+          uint32_t sr[32], pk[16];
+          load_chunk(q, lim, full, sr);
+          rs += exps(std::false_type{}, sr, nmu, pk);
+          tmem_st16(tl + col_s(x) + q * 16, pk);
+        }
+        l_run += rs;
+        tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive(B(B_PF + x));
+      }
+      mbar_wait(B(B_PV + x), (nt - 1) & 1);
+      tc_fence_after();
+    }
+    // ------------------------------------------------------ epilogue
+    uint4* dst = reinterpret_cast<uint4*>(O + ((size_t)h * N + pos) * D);
+    if (nt > 0) {
+      const float inv = l_run > 0.f ? pend_alpha / l_run : 0.f;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint32_t o[32];
+        __syncwarp();
+        tmem_ld32(tl + col_o(x) + q * 32, o);
+        tmem_wait_ld();
+        if (rvalid && l_run > 0.f) {
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const float* f = reinterpret_cast<const float*>(o + 8 * c);
+            dst[q * 4 + c] = make_uint4(pack_bf16x2(f[0] * inv, f[1] * inv), pack_bf16x2(f[2] * inv, f[3] * inv),
+                                        pack_bf16x2(f[4] * inv, f[5] * inv), pack_bf16x2(f[6] * inv, f[7] * inv));
+          }
+        }
+      }
+    }
+    if (rvalid) {
+      if (l_run > 0.f) {
+        if (lse) lse[(size_t)h * N + pos] = static_cast<float>(M_LN2) * (m_run + log2f(l_run));
+      } else {
+        const uint4* src = reinterpret_cast<const uint4*>(Vorig + ((size_t)g * N + sink) * D);
+#pragma unroll
+        for (int c = 0; c < 16; ++c) dst[c] = __ldg(src + c);
+        if (lse) lse[(size_t)h * N + pos] = -INFINITY;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    __syncwarp();
+    tc_fence_after();
+    tmem_dealloc(tmem, TMEM_COLS);
+  }
+}
+
+template <int POLY>
+__global__ void __launch_bounds__(rpt::NTHREADS, 1)
+sparse_fwd_rpt_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
+                      const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __restrict__ Vorig,
+                      const int32_t* __restrict__ rows, const int32_t* __restrict__ counts,
+                      const int32_t* __restrict__ sel, const int32_t* __restrict__ sel_counts, int Hq, int rep, int N,
+                      int cap, int sel_stride, int sink, __nv_bfloat16* __restrict__ O, float* __restrict__ lse,
+                      int* __restrict__ status) {
+  fwd_tile_rpt<POLY>(blockIdx.x, tm_k, tm_v, Q, Vorig, rows, counts, sel, sel_counts, Hq, rep, N, cap, sel_stride,
+                     sink, O, lse, status);
+}
+#endif  // OMNI_VARIANTS
+
 }  // namespace fwd
 }  // namespace omni
 
@@ -623,6 +974,35 @@ extern "C" int omni_sparse_attn_fwd_ex(const void* Q, const void* K_sel, const v
     const char* e = getenv("OMNI_FWD_POLY");
     return e ? atoi(e) : kDefaultPoly;
   }();
+  static const bool rpt_impl = [] {
+    const char* e = getenv("OMNI_FWD_IMPL");
+    return e && strcmp(e, "rpt") == 0;
+  }();
+  if (rpt_impl && status != nullptr) {
+    CUtensorMap tk, tv;
+    int st = omni_make_tmap_rows(&tk, K_sel, (uint64_t)n_kv_heads * cap, 128, 2, 64, fwd::BN);
+    if (st) return st;
+    st = omni_make_tmap_rows(&tv, V_sel, (uint64_t)n_kv_heads * cap, 128, 2, 64, fwd::BN);
+    if (st) return st;
+    auto kern = fwd::sparse_fwd_rpt_kernel<kDefaultPoly>;
+    auto redo = fwd::sparse_fwd_kernel<kDefaultPoly, false, false, true>;
+    OMNI_CUDA_TRY(omni_smem_attr(kern, (int)fwd::SMEM_BYTES));
+    OMNI_CUDA_TRY(omni_smem_attr(redo, (int)fwd::SMEM_BYTES));
+    const int n_tiles = (seq_len + 2 * fwd::BM - 1) / (2 * fwd::BM);
+    const int rep = n_q_heads / n_kv_heads;
+    OMNI_CUDA_TRY(cudaMemsetAsync(status, 0, sizeof(int32_t), st_));
+    kern<<<n_tiles * n_q_heads, fwd::rpt::NTHREADS, fwd::SMEM_BYTES, st_>>>(
+        tk, tv, static_cast<const __nv_bfloat16*>(Q), static_cast<const __nv_bfloat16*>(V), rows, counts, selected,
+        sel_counts, n_q_heads, rep, seq_len, cap, seq_len, sink_index, static_cast<__nv_bfloat16*>(O), lse, status);
+    int dev = 0, sms = 148;
+    OMNI_CUDA_TRY(cudaGetDevice(&dev));
+    OMNI_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    redo<<<std::min<unsigned>(n_tiles * n_q_heads, (unsigned)sms), fwd::NTHREADS, fwd::SMEM_BYTES, st_>>>(
+        tk, tv, static_cast<const __nv_bfloat16*>(Q), static_cast<const __nv_bfloat16*>(V), rows, counts, selected,
+        sel_counts, n_q_heads, rep, seq_len, cap, seq_len, sink_index, n_tiles, static_cast<__nv_bfloat16*>(O), lse,
+        nullptr, status);
+    return omni_launch_check();
+  }
   if (!single)
     return omni_sparse_attn_fwd_pair(Q, K_sel, V_sel, V, rows, counts, selected, sel_counts, n_q_heads, n_kv_heads,
                                      seq_len, cap, sink_index, O, lse, poly_env, st_);

@@ -124,8 +124,12 @@ __global__ void __launch_bounds__(256) probe_mass_fused_kernel(const double* __r
   double* skb = sq + PF_ROWS * ld;    // [2][64][ld]: key tiles, double-buffered
   double* S = skb + 2 * PF_JT * ld;   // [16][nb]
   __shared__ double s_m[PF_ROWS], s_l[PF_ROWS];
-  const int h = blockIdx.y, g = h / rep;
-  const int I0 = blockIdx.x * PF_ROWS;
+  // heaviest row tiles (most visible key blocks) first across all heads: the
+  // light tiles fill the tail of the launch (longest-processing-time order)
+  const int hq = gridDim.y, ntiles = gridDim.x;
+  const int t = ntiles - 1 - (int)((blockIdx.y * gridDim.x + blockIdx.x) / hq);
+  const int h = (int)((blockIdx.y * gridDim.x + blockIdx.x) % hq), g = h / rep;
+  const int I0 = t * PF_ROWS;
   const int jmax = min(nb, I0 + PF_ROWS);  // key blocks visible to the CTA's last row
   const double scale = 1.0 / sqrt(static_cast<double>(d));
   // global -> shared copies as 16-byte cp.async (all of a thread's chunks in
@@ -199,7 +203,7 @@ __global__ void __launch_bounds__(256) probe_mass_fused_kernel(const double* __r
   }
   __syncthreads();
   // partial column sums of the normalised rows (fixed row order)
-  double* out = partial + ((size_t)h * gridDim.x + blockIdx.x) * nb;
+  double* out = partial + ((size_t)h * ntiles + t) * nb;
   for (int J = threadIdx.x; J < jmax; J += blockDim.x) {
     double t = 0.0;
     for (int ii = max(0, J - I0); ii < PF_ROWS; ++ii) {

@@ -73,7 +73,9 @@ for _g in range(K.shape[0]):
                                                  ("single", "8", "1", False), ("single", "4", "0", False),
                                                  ("single", "4", "1", True), ("single", "4", "0", True),
                                                  ("single", "6", "1", "ramp"), ("single", "6", "0", "ramp"),
-                                                 ("pair", "0", "1", False), ("pair", "4", "1", False)])
+                                                 ("pair", "0", "1", False), ("pair", "4", "1", False),
+                                                 ("rpt", "6", "1", False), ("rpt", "6", "1", True),
+                                                 ("rpt", "6", "1", "ramp")])
 def test_forward_variant_matches_oracle(impl, poly, fast, jump):
     env = dict(os.environ, OMNI_FWD_IMPL=impl, OMNI_FWD_POLY=poly, OMNI_FWD_FAST=fast,
                OMNI_LIBRARY=os.path.join(ROOT, "paper_2511_12201_b200", "lib", "libomnisparse_variants.so"))
@@ -85,6 +87,6 @@ def test_forward_variant_matches_oracle(impl, poly, fast, jump):
     r = json.loads(out.stdout.strip().splitlines()[-1])
     assert not r["nan"]
     assert r["scaled_err"] <= 1.0, r  # |err| <= 0.02 + 0.02 |ref| (bf16 P, fp32 accumulation)
-    if impl == "single" and fast == "1":
+    if impl in ("single", "rpt") and fast == "1":
         # the fast kernel hands over to the safe re-run exactly when a logit jump exceeds 2^64
         assert r["fallback"] == (1 if jump is True else 0), r
