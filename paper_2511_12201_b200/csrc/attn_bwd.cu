@@ -129,18 +129,22 @@ constexpr int NSK = 3;
 constexpr uint32_t OFF_Q = 0, OFF_DO = TILE, OFF_K = 2 * TILE, OFF_V = OFF_K + NSK * TILE;
 constexpr uint32_t OFF_BAR = OFF_V + 2 * TILE;
 enum { B_QD = 0, B_KF = 1, B_KE = 1 + NSK, B_VF = 1 + 2 * NSK, B_VE = 3 + 2 * NSK, B_SF = 5 + 2 * NSK, B_SE, B_DSF,
-       B_DSE, B_N };
+       B_DSE, B_QT, B_N };
 constexpr uint32_t OFF_TMEM = OFF_BAR + 8 * B_N;
 constexpr uint32_t SMEM = OFF_TMEM + 16 + 1024;
 // dS (bf16 pairs, 64 columns) lives in TMEM: dQ += dS K is a TS MMA, so
 // the only shared-memory operand traffic of a key tile is S / dP's and K's
 // (the SS dS product made the kernel shared-memory-bandwidth bound)
 constexpr uint32_t COL_S = 0, COL_DP = 128, COL_DQ = 256, COL_DS = 384;
+// QT: the Q tile also lives in TMEM (bf16 pairs, columns 448..511), so
+// S = Q K^T is a TS MMA too and only K crosses the shared-memory operand
+// path for it (the SS S / dP MMAs bound the MMA pipeline at 128 B/clk)
+constexpr uint32_t COL_Q = 448;
 }  // namespace dq
 
 // PROBE (profiling only, OMNI_DQ_PROBE=1): the gradient warps release dS
 // without computing it (the MMA / TMA pipeline floor).
-template <int PROBE>
+template <int PROBE, bool QT = true>
 __global__ void __launch_bounds__(576, 1)
 dq_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
           const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
@@ -184,6 +188,7 @@ dq_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
     mbar_init(B(B_SE), 512);
     mbar_init(B(B_DSF), 512);
     mbar_init(B(B_DSE), 1);
+    mbar_init(B(B_QT), 512);
     fence_mbar_init();
   }
   if (warp == 1) {
@@ -235,7 +240,8 @@ dq_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
           const uint32_t off = ((kk >> 2) * ATOM + (kk & 3) * 32) >> 4;
-          umma_bf16_ws(tmem + COL_S, dq0 + off, dk0 + ((sk * TILE) >> 4) + off, id_kk, kk > 0);
+          if constexpr (QT) umma_bf16_ts_ws(tmem + COL_S, tmem + COL_Q + kk * 8, dk0 + ((sk * TILE) >> 4) + off, id_kk, kk > 0);
+          else umma_bf16_ws(tmem + COL_S, dq0 + off, dk0 + ((sk * TILE) >> 4) + off, id_kk, kk > 0);
         }
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
@@ -246,6 +252,8 @@ dq_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
         umma_commit_ws(B(B_SF));
       };
       mbar_wait(B(B_QD), 0);
+      if constexpr (QT) mbar_wait(B(B_QT), 0);  // Q copied into TMEM by the gradient warps
+      tc_fence_after();
       issue_s(0);
       for (int j = 0; j < nt; ++j) {
         mbar_wait(B(B_SE), j & 1);
@@ -278,6 +286,22 @@ dq_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
     const float sl2 = static_cast<float>(kLog2e / sqrt(static_cast<double>(D)));
     const uint64_t c2 = f32x2(sl2, sl2), nl2 = f32x2(-l2, -l2), nD2 = f32x2(-Dv, -Dv);
     const Exp2PolyConsts pc = exp2_poly_consts();
+    if (QT && nt > 0) {
+      // row i of the Q tile (swizzled smem, TMA) -> TMEM lane i: this warp's
+      // 32 elements 32 hf .. 32 hf + 31 as 16 bf16-pair columns
+      mbar_wait(B(B_QD), 0);
+      uint32_t qw[16];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const uint4 v = *reinterpret_cast<const uint4*>(smem + OFF_Q + (hf >> 1) * ATOM + swz(i, (hf & 1) * 4 + c));
+        qw[4 * c] = v.x; qw[4 * c + 1] = v.y; qw[4 * c + 2] = v.z; qw[4 * c + 3] = v.w;
+      }
+      __syncwarp();
+      tmem_st16(tl + COL_Q + hf * 16, qw);
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(B(B_QT));
+    }
     for (int j = 0; j < nt; ++j) {
       mbar_wait(B(B_SF), j & 1);
       tc_fence_after();
@@ -1084,12 +1108,17 @@ extern "C" int omni_sparse_attn_bwd_ex(const void* Q, const void* K_sel, const v
   const int n_tiles = capq / 128;
 #ifdef OMNI_VARIANTS
   OMNI_CUDA_TRY(omni_smem_attr(bwd::dq_kernel<1>, (int)bwd::dq::SMEM));
+  OMNI_CUDA_TRY(omni_smem_attr(bwd::dq_kernel<0, false>, (int)bwd::dq::SMEM));
   OMNI_CUDA_TRY(omni_smem_attr(bwd::dkv_kernel, (int)bwd::dkv::SMEM));
   static const int dq_probe = [] {
     const char* e = getenv("OMNI_DQ_PROBE");
     return e ? atoi(e) : 0;
   }();
-  auto dq_kern = dq_probe == 1 ? bwd::dq_kernel<1> : bwd::dq_kernel<0>;
+  static const bool dq_qt = [] {  // OMNI_DQ_QT=0: Q read from shared memory by the S MMA
+    const char* e = getenv("OMNI_DQ_QT");
+    return !(e && atoi(e) == 0);
+  }();
+  auto dq_kern = dq_probe == 1 ? bwd::dq_kernel<1> : dq_qt ? bwd::dq_kernel<0> : bwd::dq_kernel<0, false>;
 #else
   auto dq_kern = bwd::dq_kernel<0>;
 #endif
