@@ -463,17 +463,6 @@ constexpr uint32_t SP_STAGE = 256 * 256;  // one probe block of bf16 rows, d = 1
 __device__ __forceinline__ float bf_lo(uint32_t w) { return __uint_as_float(w << 16); }
 __device__ __forceinline__ float bf_hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
 
-// Exact bf16 -> float64 on the integer pipes (F2F.F64.F32 issues to the XU
-// pipe, whose conversion rate made it the limiter of K1 / K2: 66 % busy).
-// f = the value's fp32 bits (low 16 bits zero). For a normal number the
-// float64 high word is sign | (exp8 + 896) << 20 | mant7 << 13 and the low
-// word is 0; +-0 keeps just the sign. Denormal / inf / nan bf16 values are
-// flagged (*odd) and converted by the caller with the hardware instruction.
-__device__ __forceinline__ double bf32_to_f64(uint32_t f) {
-  const uint32_t a = f & 0x7FFFFFFFu;
-  const uint32_t hi = a != 0u ? (((a >> 3) + 0x38000000u) | (f & 0x80000000u)) : f;
-  return __hiloint2double(static_cast<int>(hi), 0);
-}
 
 // item -> (head, block) and its row span
 struct SpItem {
@@ -543,13 +532,23 @@ __global__ void __launch_bounds__(QP_WARPS * 32, 1) q_score_stream_kernel(
     __nv_bfloat16* __restrict__ o_zero) {
   constexpr int d = 128;
   extern __shared__ __align__(1024) uint8_t sp_smem[];
+  static_assert(QP_SLABS == 2, "the mbarrier hand-off needs the double-buffered slab");
   __shared__ __align__(8) uint64_t bars[SP_STAGES];
+  // done[sl]: every warp has consumed its rows of the item and written its
+  // slab column sums (QP_WARPS arrivals); sfree[sl]: the four reducer warps
+  // have read the slab (4 arrivals). No CTA-wide barrier per item: warps
+  // drift across items, bounded by the ring and the slab double buffer.
+  __shared__ __align__(8) uint64_t done[2], sfree[2];
   __shared__ int s_cnt[QP_SLABS][QP_WARPS];
   double* s_pool = reinterpret_cast<double*>(sp_smem + SP_STAGES * SP_STAGE);  // [slabs][warps][128]
   const uint32_t ring = smem_u32(sp_smem);
   const int G = gridDim.x;
   if (threadIdx.x == 0) {
     for (int s = 0; s < SP_STAGES; ++s) mbar_init(smem_u32(&bars[s]), 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(smem_u32(&done[b]), QP_WARPS);
+      mbar_init(smem_u32(&sfree[b]), 4);
+    }
     fence_mbar_init();
     for (int k = 0; k < SP_STAGES; ++k) {
       const int i = blockIdx.x + k * G;
@@ -671,26 +670,31 @@ __global__ void __launch_bounds__(QP_WARPS * 32, 1) q_score_stream_kernel(
         for (int c = 0; c < per; ++c) orow[c] = make_uint4(0, 0, 0, 0);
       }
     }
-    const int sl = QP_SLABS == 2 ? (k & 1) : 0;
+    const int sl = k & 1;
     double* slab = s_pool + (size_t)sl * QP_WARPS * d;
+    cnt = warp_sum(cnt);
+    if (k >= 2) mbar_wait(smem_u32(&sfree[sl]), ((k >> 1) - 1) & 1);  // item k - 2's slab read
     *reinterpret_cast<double2*>(slab + warp * d + 4 * lane) = make_double2(pool[0], pool[1]);
     *reinterpret_cast<double2*>(slab + warp * d + 4 * lane + 2) = make_double2(pool[2], pool[3]);
-    cnt = warp_sum(cnt);
     if (lane == 0) s_cnt[sl][warp] = cnt;
-    __syncthreads();  // stage s consumed, slab complete
-    if (threadIdx.x == 0 && i + SP_STAGES * G < n_items)
-      sp_issue(Q, nb, block, N, i + SP_STAGES * G, ring + s * SP_STAGE, smem_u32(&bars[s]));
-    if (threadIdx.x < d) {
+    __syncwarp();
+    if (lane == 0) mbar_arrive(smem_u32(&done[sl]));  // (release: this warp's slab writes and smem reads)
+    if (warp < 4) {  // reducers: the item's column sums over the warps in a fixed order
+      mbar_wait(smem_u32(&done[sl]), (k >> 1) & 1);
+      if (threadIdx.x == 0 && i + SP_STAGES * G < n_items)  // every warp is done with stage s
+        sp_issue(Q, nb, block, N, i + SP_STAGES * G, ring + s * SP_STAGE, smem_u32(&bars[s]));
       double t = 0.0;
 #pragma unroll
       for (int w = 0; w < QP_WARPS; ++w) t += slab[w * d + threadIdx.x];
       pooled_q[((size_t)h * nb + it.J) * d + threadIdx.x] = t / static_cast<double>(nr);
-    } else if (threadIdx.x == d) {
-      int t = 0;
-      for (int w = 0; w < QP_WARPS; ++w) t += s_cnt[sl][w];
-      block_active[(size_t)h * nb + it.J] = t;
+      if (threadIdx.x == 0) {
+        int c = 0;
+        for (int w = 0; w < QP_WARPS; ++w) c += s_cnt[sl][w];
+        block_active[(size_t)h * nb + it.J] = c;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&sfree[sl]));
     }
-    if (QP_SLABS == 1) __syncthreads();  // slab and counts read before the next item writes them
   }
 }
 
