@@ -1,11 +1,17 @@
 // K1 (probe keys + pooled K), K2 (query classification + pooled Q + lazy-row
 // zeroing), active-row compaction and K6 row gather.
 //
-// All four are HBM-bound streaming passes: K1 and K2 read K / Q exactly once
-// with 16-byte (bf16 x 8) or 32-byte (f32 x 8) vector loads, accumulate in
-// float64 (decision-critical, SURVEY §7 hard parts) and write only tiny
-// outputs. One CTA per (probe block, head): grid = nb x H, which at 64K tokens
-// is 256 x 28 = 7168 CTAs (48 waves of 148 SMs).
+// All four are HBM-bound streaming passes that read K / Q exactly once and
+// accumulate the decision-critical sums in float64 (SURVEY §7 hard parts).
+// The bf16 / d = 128 hot path (K1 kv_probe_stream_kernel, K2
+// q_score_stream_kernel) runs one persistent CTA per SM over a 3-stage
+// bulk-copy ring of probe blocks; the generic kernels (one CTA per (probe
+// block, head)) serve other dtypes, head sizes, the want_prob path and the
+// A/B switch OMNI_QSCORE_F64. Measured at 64K tokens (28 / 4 heads, one
+// B200, profiles/r02_notes.md): K1 0.024 ms (2.8 TB/s), K2 0.177 ms (3.9
+// TB/s, 0.60 of the measured copy bandwidth; the float64 column sums of the
+// pooled queries keep it issue-bound) vs 0.028 / 0.194 ms for the generic
+// kernels.
 #include "common.cuh"
 
 namespace omni {
