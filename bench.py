@@ -455,7 +455,12 @@ def train_section(args, steps, warmup, tc_peak):
         res["roofline"] = {"bound": "tensor", "kernel": "K5 backward (bwd_prep + dq_kernel + dkv2_kernel)",
                            "achieved": ach, "peak": tc_peak, "unit": "TFLOP/s", "frac": ach / tc_peak,
                            "algorithmic_flops_per_launch": 2.5 * fwd_flops, "launch_ms": bwd_ms,
-                           "traffic": None, "ncu": "profiles/r02_ncu_k5_details.txt"}
+                           "traffic": None, "ncu": "profiles/r02_ncu_k5_details.txt",
+                           # the kernels execute 7 GEMMs per visible tile pair (dq recomputes S and dP; the
+                           # fifth 128x128 fp32 accumulator a fused dq+dkv needs does not fit in TMEM beside
+                           # S^T, dP^T, dK, dV): executed FLOPs = 3.5 x forward, against the same peak
+                           "executed_flops_per_launch": 3.5 * fwd_flops,
+                           "frac_executed": 3.5 * fwd_flops / (bwd_ms / 1e3) / 1e12 / tc_peak}
         res["forward_roofline"] = {"achieved": fwd_flops / (fwd_ms / 1e3) / 1e12, "unit": "TFLOP/s",
                                    "frac": fwd_flops / (fwd_ms / 1e3) / 1e12 / tc_peak, "launch_ms": fwd_ms}
         del K_sel, V_sel, O, lse
