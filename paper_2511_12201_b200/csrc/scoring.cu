@@ -540,10 +540,11 @@ __global__ void __launch_bounds__(QP_WARPS * 32, 1) q_score_stream_kernel(
   extern __shared__ __align__(1024) uint8_t sp_smem[];
   static_assert(QP_SLABS == 2, "the mbarrier hand-off needs the double-buffered slab");
   __shared__ __align__(8) uint64_t bars[SP_STAGES];
-  // done[sl]: every warp has consumed its rows of the item and written its
-  // slab column sums (QP_WARPS arrivals); sfree[sl]: the four reducer warps
-  // have read the slab (4 arrivals). No CTA-wide barrier per item: warps
-  // drift across items, bounded by the ring and the slab double buffer.
+  // done[sl]: every thread has consumed its rows of the item and written its
+  // slab column sums (one arrival per thread, so each thread's own accesses
+  // are released by its own arrive); sfree[sl]: the 128 reducer threads have
+  // read the slab. No CTA-wide barrier per item: warps drift across items,
+  // bounded by the ring and the slab double buffer.
   __shared__ __align__(8) uint64_t done[2], sfree[2];
   __shared__ int s_cnt[QP_SLABS][QP_WARPS];
   double* s_pool = reinterpret_cast<double*>(sp_smem + SP_STAGES * SP_STAGE);  // [slabs][warps][128]
@@ -552,8 +553,8 @@ __global__ void __launch_bounds__(QP_WARPS * 32, 1) q_score_stream_kernel(
   if (threadIdx.x == 0) {
     for (int s = 0; s < SP_STAGES; ++s) mbar_init(smem_u32(&bars[s]), 1);
     for (int b = 0; b < 2; ++b) {
-      mbar_init(smem_u32(&done[b]), QP_WARPS);
-      mbar_init(smem_u32(&sfree[b]), 4);
+      mbar_init(smem_u32(&done[b]), QP_WARPS * 32);
+      mbar_init(smem_u32(&sfree[b]), 128);
     }
     fence_mbar_init();
     for (int k = 0; k < SP_STAGES; ++k) {
@@ -683,8 +684,7 @@ __global__ void __launch_bounds__(QP_WARPS * 32, 1) q_score_stream_kernel(
     *reinterpret_cast<double2*>(slab + warp * d + 4 * lane) = make_double2(pool[0], pool[1]);
     *reinterpret_cast<double2*>(slab + warp * d + 4 * lane + 2) = make_double2(pool[2], pool[3]);
     if (lane == 0) s_cnt[sl][warp] = cnt;
-    __syncwarp();
-    if (lane == 0) mbar_arrive(smem_u32(&done[sl]));  // (release: this warp's slab writes and smem reads)
+    mbar_arrive(smem_u32(&done[sl]));  // releases this thread's slab writes and stage reads
     if (warp < 4) {  // reducers: the item's column sums over the warps in a fixed order
       mbar_wait(smem_u32(&done[sl]), (k >> 1) & 1);
       if (threadIdx.x == 0 && i + SP_STAGES * G < n_items)  // every warp is done with stage s
@@ -698,8 +698,7 @@ __global__ void __launch_bounds__(QP_WARPS * 32, 1) q_score_stream_kernel(
         for (int w = 0; w < QP_WARPS; ++w) c += s_cnt[sl][w];
         block_active[(size_t)h * nb + it.J] = c;
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(smem_u32(&sfree[sl]));
+      mbar_arrive(smem_u32(&sfree[sl]));
     }
   }
 }

@@ -1,6 +1,7 @@
 """Small-shape runs of the warp-specialised mbarrier / TMEM kernels for
 compute-sanitizer racecheck / synccheck (r02): K4 forward (fast + safe),
-K5 backward (bwd_prep, dq, dkv2), K7 paged decode, at sizes where the tools
+K5 backward (bwd_prep, dq with Q in TMEM, dkv2), K7 paged decode, and the
+K1 / K2 persistent stream kernels, at sizes where the tools
 finish in minutes (GQA 8 / 2 heads, ragged N)."""
 import sys
 
@@ -30,5 +31,12 @@ means = [unit_vision_mean(K, nv)]
 for t in range(2):
     gdec.decode_attention_batch(decode_queries_device(8, 2, means, [0], 0.5, t), cache, 0.08)
     gdec.append_answer_batch(cache, torch.randn(1, 2, 128, device="cuda"), torch.randn(1, 2, 128, device="cuda"))
+# K1 / K2 persistent streams with several items per CTA (ring wrap-around,
+# slab double buffer, mbarrier hand-offs): 16K tokens, 8 Q / 2 KV heads =
+# 512 K2 items over at most 148 CTAs
+Qs, Ks, _ = generate_device(8, 2, 128, 16384 - 64, 64, seed=2)
+kl, ka, _ = ops.kv_probe(Ks, 16384 - 64, 0, 256)
+Oz = torch.empty_like(Qs)
+ops.q_score(Qs, kl, ka, 16384 - 64, 0.08, True, 256, O_zero=Oz)
 torch.cuda.synchronize()
 print("ok")
