@@ -1074,6 +1074,26 @@ extern "C" int omni_sparse_attn_fwd_ex(const void* Q, const void* K_sel, const v
   auto qp = static_cast<const __nv_bfloat16*>(Q);
   auto vp = static_cast<const __nv_bfloat16*>(V);
   auto op = static_cast<__nv_bfloat16*>(O);
+#ifdef OMNI_VARIANTS
+  // profiling (OMNI_FWD_PERSIST_SAFE=1): the safe kernel as a persistent
+  // grid-stride loop (the redo instance, one CTA per SM) instead of one CTA
+  // per tile pair — isolates the per-CTA launch cost
+  static const bool persist_safe = [] {
+    const char* e = getenv("OMNI_FWD_PERSIST_SAFE");
+    return e && atoi(e) != 0;
+  }();
+  if (persist_safe && status != nullptr) {
+    const int one = 1;
+    OMNI_CUDA_TRY(cudaMemcpyAsync(status, &one, sizeof(int32_t), cudaMemcpyHostToDevice, st_));
+    int dev = 0, sms = 148;
+    OMNI_CUDA_TRY(cudaGetDevice(&dev));
+    OMNI_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    redo<<<std::min<unsigned>(grid.x, (unsigned)sms), fwd::NTHREADS, fwd::SMEM_BYTES, st_>>>(
+        tk, tv, qp, vp, rows, counts, selected, sel_counts, n_q_heads, rep, seq_len, cap, seq_len, sink_index, n_tiles,
+        op, lse, nullptr, status);
+    return omni_launch_check();
+  }
+#endif
   if (use_fast) {
     OMNI_CUDA_TRY(cudaMemsetAsync(status, 0, sizeof(int32_t), st_));
     fast<<<grid, fwd::NTHREADS, fwd::SMEM_BYTES, st_>>>(tk, tv, qp, vp, rows, counts, selected, sel_counts, n_q_heads,
