@@ -623,13 +623,17 @@ def run_ours(args):
         line["parity"] = par
         line["breakdown_ms"] = {"select_path_K1_K2_compact_K3": sel_ms, "gather_K6": gat_ms, "sparse_fa_K4": fa_ms,
                                 "k4_share_of_step": fa_ms / ms}
-        # ----- HBM-bound kernels against the measured copy bandwidth (algorithmic bytes)
+        # ----- HBM-bound kernels against the measured copy bandwidth (algorithmic bytes),
+        # each timed alone (the burst peak's condition): after an idle second,
+        # so they do not inherit the power state of the tensor-bound step above
         try:
             hb = {}
-            k1_ms = time_cuda(lambda: ops.kv_probe(K, nv, 0, 256), args.steps, 2)
+            torch.cuda.synchronize()
+            time.sleep(1.0)
+            k1_ms = time_cuda(lambda: ops.kv_probe(K, nv, 0, 256), max(args.steps, 30), 3)
             k1_bytes = HKV * n * D * 2
             kl_, ka_, _ = ops.kv_probe(K, nv, 0, 256)
-            k2_ms = time_cuda(lambda: ops.q_score(Q, kl_, ka_, nv, args.tau, True, 256, O_zero=O), args.steps, 2)
+            k2_ms = time_cuda(lambda: ops.q_score(Q, kl_, ka_, nv, args.tau, True, 256, O_zero=O), max(args.steps, 30), 3)
             lazy_rows = int((res.active == 0).sum())
             k2_bytes = HQ * n * D * 2 + lazy_rows * D * 2 + HQ * n  # Q read, lazy O rows zeroed, flags
             bsum = int(sel.info[4:].sum())
