@@ -415,10 +415,11 @@ def train_section(args, steps, warmup, tc_peak):
     V.requires_grad_(True)
     dO = torch.randn_like(Q)
 
-    def sparse_step():
+    def sparse_step():  # = autograd.sparse_attention (the public API), keeping the plan for the FLOP count
+        out = torch.empty(Q.shape, device=Q.device, dtype=torch.bfloat16)
         with torch.no_grad():
-            _, _, _, _, _, _, rows, counts, _, sel = select_device(Q.detach(), K.detach(), nv, cfg)
-        O = SparseAttentionFn.apply(Q, K, V, plan_from_selection(rows, counts, sel, 0))
+            _, _, _, _, _, _, rows, counts, _, sel = select_device(Q.detach(), K.detach(), nv, cfg, O_zero=out)
+        O = SparseAttentionFn.apply(Q, K, V, plan_from_selection(rows, counts, sel, 0, out))
         O.backward(dO)
         return rows, counts, sel
 

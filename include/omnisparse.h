@@ -191,6 +191,18 @@ int omni_slim_cache(const void* K, const void* V, int dtype, int n_kv_heads, int
 int omni_scatter_rows(const void* src, int dtype, int n_groups, int src_rows, int head_dim, const int32_t* idx,
                       int idx_stride, const int32_t* counts, void* dst, int dst_rows, void* stream);
 
+/* Key-gradient epilogue of the training backward (autograd glue, no
+ * reference counterpart: slimattn has no backward): dst[g, idx[g, r]] =
+ * cast(src[g, r] + (idx[g, r] == sink_index ? sink_add[g] : 0)) for
+ * r < counts[g], src fp32 [G, src_rows, head_dim], dst (dst_dtype f32 or
+ * bf16) [G, dst_rows, head_dim] zero-initialised by the caller; when
+ * sink_add (fp32 [G, head_dim], nullable) is given and sink_index is not
+ * among a group's indices, dst[g, sink_index] = cast(sink_add[g]). idx rows
+ * ascending. One pass replaces scatter + sink add + dtype cast. */
+int omni_scatter_key_grads(const float* src, int n_groups, int src_rows, int head_dim, const int32_t* idx,
+                           int idx_stride, const int32_t* counts, int sink_index, const float* sink_add, void* dst,
+                           int dst_dtype, int dst_rows, void* stream);
+
 /* ---------------------------------------------------------------- K4
  * Gathered sparse flash-attention forward (tcgen05 + TMEM + TMA).
  * Replaces sparse_head_attention (prefill.py:89-122) for every Q head:

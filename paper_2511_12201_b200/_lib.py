@@ -48,6 +48,7 @@ SIGNATURES = {
     "omni_gather_rows": (_c_int, [_p, _c_int, _c_int, _c_int, _c_int, _p, _c_int, _p, _c_int, _p, _c_int,
                                   _c_int, _p]),
     "omni_scatter_rows": (_c_int, [_p, _c_int, _c_int, _c_int, _c_int, _p, _c_int, _p, _p, _c_int, _p]),
+    "omni_scatter_key_grads": (_c_int, [_p, _c_int, _c_int, _c_int, _p, _c_int, _p, _c_int, _p, _p, _c_int, _c_int, _p]),
     "omni_sparse_attn_fwd": (_c_int, [_p, _p, _p, _p, _p, _p, _p, _p, _c_int, _c_int, _c_int, _c_int, _c_int,
                                       _c_int, _p, _p, _p]),
     "omni_sparse_attn_fwd_ex": (_c_int, [_p, _p, _p, _p, _p, _p, _p, _p, _c_int, _c_int, _c_int, _c_int, _c_int,

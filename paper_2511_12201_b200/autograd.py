@@ -22,6 +22,10 @@ class SparsePlan:
     selected: torch.Tensor    # i32 [Hkv, N]
     sel_counts: torch.Tensor  # i32 [Hkv]
     sink_index: int
+    # optional output buffer [Hq, N, d] bf16 whose lazy rows the selection's
+    # K2 already zeroed (select_device(..., O_zero=out)): the forward then
+    # writes only the active rows instead of zero-filling the whole output
+    out: torch.Tensor | None = None
 
 
 class SparseAttentionFn(torch.autograd.Function):
@@ -32,7 +36,7 @@ class SparseAttentionFn(torch.autograd.Function):
         Qb, Kb, Vb = (x.detach().to(torch.bfloat16).contiguous() for x in (Q, K, V))
         K_sel = ops.gather_rows(Kb, plan.selected, plan.sel_counts, cap, ops.TILE)
         V_sel = ops.gather_rows(Vb, plan.selected, plan.sel_counts, cap, ops.TILE)
-        O = torch.zeros_like(Qb)
+        O = plan.out if plan.out is not None else torch.zeros_like(Qb)
         lse = torch.empty(hq, n, device=Q.device, dtype=torch.float32)
         ops.sparse_attn_fwd(Qb, K_sel, V_sel, Vb, plan.rows, plan.counts, plan.selected, plan.sel_counts,
                             plan.sink_index, O, lse)
@@ -51,17 +55,21 @@ class SparseAttentionFn(torch.autograd.Function):
         dQ, dKs, dVs, dVsink = ops.sparse_attn_bwd(Qb, K_sel, V_sel, O, dO.to(torch.bfloat16).contiguous(), lse,
                                                    plan.rows, plan.counts, plan.selected, plan.sel_counts,
                                                    dq_dtype=torch.bfloat16 if qd == torch.bfloat16 else torch.float32)
-        # compacted key gradients back to their original positions (device
-        # counts: no host round trip)
-        dK = ops.scatter_rows(dKs, plan.selected, plan.sel_counts,
-                              torch.zeros(hkv, n, Qb.shape[2], device=Qb.device, dtype=torch.float32))
-        dV = ops.scatter_rows(dVs, plan.selected, plan.sel_counts, torch.zeros_like(dK))
-        dV[:, plan.sink_index] += dVsink
-        return dQ.to(qd), dK.to(kd), dV.to(vd), None
+        # compacted key gradients back to their original positions in the
+        # leaves' dtype, the sink row's extra dV folded in before rounding
+        # (device counts: no host round trip)
+        def key_grad(src, dt, **kw):
+            tgt = dt if dt in (torch.float32, torch.bfloat16) else torch.float32
+            out = torch.zeros(hkv, n, Qb.shape[2], device=Qb.device, dtype=tgt)
+            return ops.scatter_key_grads(src, plan.selected, plan.sel_counts, out, **kw).to(dt)
+
+        dK = key_grad(dKs, kd)
+        dV = key_grad(dVs, vd, sink_index=plan.sink_index, sink_add=dVsink)
+        return dQ.to(qd), dK, dV, None
 
 
-def plan_from_selection(active_rows, counts, selection, sink_index: int) -> SparsePlan:
-    return SparsePlan(active_rows, counts, selection.selected, selection.counts, sink_index)
+def plan_from_selection(active_rows, counts, selection, sink_index: int, out: torch.Tensor | None = None) -> SparsePlan:
+    return SparsePlan(active_rows, counts, selection.selected, selection.counts, sink_index, out)
 
 
 def sparse_attention(Q: torch.Tensor, K: torch.Tensor, V: torch.Tensor, n_vision: int,
@@ -69,6 +77,8 @@ def sparse_attention(Q: torch.Tensor, K: torch.Tensor, V: torch.Tensor, n_vision
     """Differentiable OmniSparse attention for a training step: selection
     under no_grad, then the tcgen05 forward with a K5 backward."""
     check_qkv(Q, K, V)
+    # the output buffer's lazy rows are zeroed by K2 during the selection
+    out = torch.empty(Q.shape, device=Q.device, dtype=torch.bfloat16)
     with torch.no_grad():
-        _, _, _, _, _, _, rows, counts, _, sel = select_device(Q.detach(), K.detach(), n_vision, cfg)
-    return SparseAttentionFn.apply(Q, K, V, plan_from_selection(rows, counts, sel, cfg.sink_index))
+        _, _, _, _, _, _, rows, counts, _, sel = select_device(Q.detach(), K.detach(), n_vision, cfg, O_zero=out)
+    return SparseAttentionFn.apply(Q, K, V, plan_from_selection(rows, counts, sel, cfg.sink_index, out))

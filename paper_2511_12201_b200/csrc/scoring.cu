@@ -882,11 +882,68 @@ __global__ void __launch_bounds__(256) scatter_rows_kernel(const uint8_t* __rest
   }
 }
 
+// Key-gradient epilogue (training): compacted fp32 dK / dV rows to their
+// original positions in the leaves' dtype, the sink row's extra dV (rows
+// whose forward copied V[sink]) folded in before the rounding.
+__global__ void __launch_bounds__(256) scatter_key_grads_kernel(const float* __restrict__ src, int src_rows, int d,
+                                                                const int32_t* __restrict__ idx, int idx_stride,
+                                                                const int32_t* __restrict__ counts, int sink,
+                                                                const float* __restrict__ sink_add, void* dst,
+                                                                int bf16, int dst_rows) {
+  const int g = blockIdx.y;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int cnt = min(__ldg(counts + g), src_rows);
+  const int32_t* ig = idx + (size_t)g * idx_stride;
+  auto store = [&](int p, int c, float4 v) {
+    if (bf16) {
+      uint2* o = reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(dst) + ((size_t)g * dst_rows + p) * d + c);
+      *o = make_uint2(pack_bf16x2(v.x, v.y), pack_bf16x2(v.z, v.w));
+    } else {
+      *reinterpret_cast<float4*>(static_cast<float*>(dst) + ((size_t)g * dst_rows + p) * d + c) = v;
+    }
+  };
+  if (sink_add && blockIdx.x == 0 && warp == 0) {
+    // sink row not among the selected keys: it receives only the extra dV
+    const bool member = count_le(ig, cnt, sink) > (sink > 0 ? count_le(ig, cnt, sink - 1) : 0);
+    if (!member && sink >= 0 && sink < dst_rows)
+      for (int c = lane * 4; c < d; c += 128)
+        store(sink, c, __ldg(reinterpret_cast<const float4*>(sink_add + (size_t)g * d + c)));
+  }
+  for (int r = blockIdx.x * 8 + warp; r < cnt; r += gridDim.x * 8) {
+    const int p = __ldg(ig + r);
+    if (p < 0 || p >= dst_rows) continue;
+    const float* s = src + ((size_t)g * src_rows + r) * d;
+    for (int c = lane * 4; c < d; c += 128) {
+      float4 v = __ldg(reinterpret_cast<const float4*>(s + c));
+      if (sink_add && p == sink) {
+        const float4 a = __ldg(reinterpret_cast<const float4*>(sink_add + (size_t)g * d + c));
+        v.x += a.x; v.y += a.y; v.z += a.z; v.w += a.w;
+      }
+      store(p, c, v);
+    }
+  }
+}
+
 }  // namespace omni
 
 using namespace omni;
 
 static inline int nblocks(int n, int b) { return (n + b - 1) / b; }
+
+extern "C" int omni_scatter_key_grads(const float* src, int n_groups, int src_rows, int head_dim, const int32_t* idx,
+                                      int idx_stride, const int32_t* counts, int sink_index, const float* sink_add,
+                                      void* dst, int dst_dtype, int dst_rows, void* stream) {
+  omni_begin();
+  OMNI_CHECK(dst_dtype == OMNI_DTYPE_F32 || dst_dtype == OMNI_DTYPE_BF16, OMNI_E_PARAM, "key gradients must be f32 or bf16");
+  OMNI_CHECK(head_dim % 4 == 0 && head_dim >= 4, OMNI_E_SHAPE, "head_dim must be a multiple of 4");
+  OMNI_CHECK(counts != nullptr, OMNI_E_PARAM, "scatter needs device counts");
+  if (n_groups == 0 || src_rows == 0) return OMNI_OK;
+  dim3 grid(min(nblocks(src_rows, 8), 1024), n_groups);
+  scatter_key_grads_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      src, src_rows, head_dim, idx, idx_stride, counts, sink_index, sink_add, dst, dst_dtype == OMNI_DTYPE_BF16 ? 1 : 0,
+      dst_rows);
+  return omni_launch_check();
+}
 
 // OMNI_QSCORE_F64=1 (tests / A-B): the float64 q_score_bulk_kernel for every
 // row instead of the fp32-with-bound fast kernel.

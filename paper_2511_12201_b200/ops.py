@@ -243,6 +243,25 @@ def scatter_rows(src: torch.Tensor, idx: torch.Tensor, counts: torch.Tensor, out
     return out
 
 
+def scatter_key_grads(src: torch.Tensor, idx: torch.Tensor, counts: torch.Tensor, out: torch.Tensor,
+                      sink_index: int = -1, sink_add: torch.Tensor | None = None) -> torch.Tensor:
+    """out[g, idx[g, r]] = cast(src[g, r] (+ sink_add[g] at sink_index)) for
+    r < counts[g]; out (fp32 or bf16, zero-initialised) gets sink_add alone at
+    sink_index when the sink is not selected (the training backward's key
+    gradient epilogue: scatter, sink add and dtype cast in one pass)."""
+    _cuda3(src, "src")
+    _cuda3(out, "out")
+    g, rows, d = src.shape
+    if src.dtype != torch.float32 or out.shape[0] != g or out.shape[2] != d:
+        raise ShapeError("key gradient scatter takes fp32 [G, rows, d] into [G, N, d]")
+    if out.dtype not in (torch.float32, torch.bfloat16):
+        raise ShapeError("key gradients must be float32 or bfloat16")
+    sa = None if sink_add is None else sink_add.to(torch.float32).contiguous()
+    _lib.call("omni_scatter_key_grads", _p(src), g, rows, d, _p(idx), idx.shape[-1], _p(counts), int(sink_index),
+              _p(sa), _p(out), _dtype(out), out.shape[1], _stream())
+    return out
+
+
 # ----------------------------------------------------------------------- K4
 last_fwd_status: torch.Tensor | None = None
 

@@ -183,8 +183,9 @@ def sparse_attention_sharded(Q_loc: torch.Tensor, K_loc: torch.Tensor, V_loc: to
     from .autograd import SparseAttentionFn, SparsePlan
 
     check_qkv(Q_loc, K_loc, V_loc)
+    o_buf = torch.empty(Q_loc.shape, device=Q_loc.device, dtype=torch.bfloat16)  # lazy rows zeroed by K2
     with torch.no_grad():
-        out = select_sharded(Q_loc.detach(), K_loc.detach(), plan, n_vision, world, cfg, group=group)
+        out = select_sharded(Q_loc.detach(), K_loc.detach(), plan, n_vision, world, cfg, O_zero=o_buf, group=group)
     rows, counts, sel_loc, cnt_loc = out[5], out[6], out[9], out[10]
     if kv_group is not None:
         # reduce the split group's partial dK / dV in fp32, before the
@@ -192,7 +193,7 @@ def sparse_attention_sharded(Q_loc: torch.Tensor, K_loc: torch.Tensor, V_loc: to
         K_loc = ReduceGradOverGroup.apply(K_loc.float(), kv_group)
         V_loc = ReduceGradOverGroup.apply(V_loc.float(), kv_group)
     return SparseAttentionFn.apply(Q_loc, K_loc, V_loc, SparsePlan(rows, counts, sel_loc.contiguous(),
-                                                                   cnt_loc.contiguous(), cfg.sink_index))
+                                                                   cnt_loc.contiguous(), cfg.sink_index, o_buf))
 
 
 # ------------------------------------------------------------------ decode
