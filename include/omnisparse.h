@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define OMNI_ABI_VERSION 2
+#define OMNI_ABI_VERSION 3
 
 enum omni_status {
   OMNI_OK = 0,

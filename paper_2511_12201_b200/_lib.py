@@ -87,7 +87,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
-    if lib.omni_abi_version() != 2:
+    if lib.omni_abi_version() != 3:
         raise CudaError("libomnisparse ABI version mismatch")
     _lib = lib
     return lib

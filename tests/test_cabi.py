@@ -24,7 +24,7 @@ def test_library_exports_every_declared_symbol():
     for s in syms:
         assert hasattr(lib, s), f"{s} declared in omnisparse.h but not exported"
         assert s in _lib.SIGNATURES, f"{s} has no ctypes prototype"
-    assert lib.omni_abi_version() == 2
+    assert lib.omni_abi_version() == 3
 
 
 def test_workspace_queries_run_without_gpu():
