@@ -90,6 +90,18 @@ __device__ __forceinline__ constexpr bool use_poly(int pair) {
 // lane 0 of every softmax / MMA warp, read back with omni_debug_fwd_trace.
 __device__ unsigned long long g_fwd_trace[8];
 
+#ifdef OMNI_FWD_CTA_TIMING
+// Profiling build only (VFLAGS=-DOMNI_FWD_CTA_TIMING, profiles/k4_cta_timing.py):
+// per-CTA wall-clock phases of the fast kernel in ns (globaltimer), summed
+// into g_fwd_trace: [0] start -> first QK issued (prologue), [1] tile A's
+// last PV complete -> exit (epilogue), [2] start -> exit, [3] CTAs.
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#endif
+
 // FAST: deferred agreement between the two halves of a row (see the tile loop);
 // a tile whose logits jump by more than 2^64 over the running max sets
 // *status and the launch is redone by the FAST = false kernel (only_if).
@@ -104,6 +116,10 @@ __device__ __forceinline__ void fwd_tile(int L, bool reuse, const CUtensorMap& t
                                          __nv_bfloat16* __restrict__ O, float* __restrict__ lse,
                                          int* __restrict__ status) {
   extern __shared__ uint8_t smem_raw[];
+#ifdef OMNI_FWD_CTA_TIMING
+  const unsigned long long t_start = gtimer();
+  __shared__ unsigned long long s_t_first, s_t_last;
+#endif
   const int h = L % Hq;
   // Heaviest (latest rows) tile pairs first, counted down from the largest
   // active-row count over the heads (device-side: the grid is sized for N
@@ -232,6 +248,9 @@ __device__ __forceinline__ void fwd_tile(int L, bool reuse, const CUtensorMap& t
         if (nt[x] == 0) continue;
         mbar_wait(B(B_QF + x), 0);
         tc_fence_after();
+#ifdef OMNI_FWD_CTA_TIMING
+        if (x == 0 && lane == 0) s_t_first = gtimer();
+#endif
         qk(x, 0);
       }
       umma_commit_ws(B(B_KE + 0));
@@ -502,6 +521,9 @@ __device__ __forceinline__ void fwd_tile(int L, bool reuse, const CUtensorMap& t
       }
       mbar_wait(B(B_PV + x), (nt - 1) & 1);
       tc_fence_after();
+#ifdef OMNI_FWD_CTA_TIMING
+      if (threadIdx.x == 64) s_t_last = gtimer();  // (a tile-A thread)
+#endif
       // the row normaliser is the sum of both halves' partial sums
       s_xch[x][i][hf] = l_run;
       named_bar_sync(bid, 2 * 32);
@@ -546,6 +568,15 @@ __device__ __forceinline__ void fwd_tile(int L, bool reuse, const CUtensorMap& t
     tc_fence_after();
     tmem_dealloc(tmem, TMEM_COLS);
   }
+#ifdef OMNI_FWD_CTA_TIMING
+  if (FAST && threadIdx.x == 0 && ntm > 0) {
+    const unsigned long long t_end = gtimer();
+    atomicAdd(&g_fwd_trace[0], s_t_first - t_start);
+    atomicAdd(&g_fwd_trace[1], t_end - s_t_last);
+    atomicAdd(&g_fwd_trace[2], t_end - t_start);
+    atomicAdd(&g_fwd_trace[3], 1ull);
+  }
+#endif
   if (reuse) {  // the next tile re-initialises the barriers
     __syncthreads();
     if (threadIdx.x == 0)
