@@ -17,25 +17,6 @@ import torch
 from . import ops
 from .errors import LayoutError, ParameterError, ShapeError
 
-_SIDE: dict = {}
-
-
-def _side_stream(device) -> torch.cuda.Stream:
-    """One auxiliary stream per device for the prefill's independent launches
-    (row compaction beside K3, the V gather beside the K gather)."""
-    idx = torch.device(device).index
-    idx = torch.cuda.current_device() if idx is None else idx
-    if idx not in _SIDE:
-        _SIDE[idx] = torch.cuda.Stream(device=idx)
-    return _SIDE[idx]
-
-
-def _fork(device):
-    """Side stream ordered after everything queued so far on the current one."""
-    side = _side_stream(device)
-    side.wait_stream(torch.cuda.current_stream(device))
-    return side
-
 
 @dataclass(frozen=True)
 class SparsityConfig:
@@ -107,13 +88,7 @@ def select_device(Q: torch.Tensor, K: torch.Tensor, n_vision: int, cfg: Sparsity
     k_lazy, k_act, pk = ops.kv_probe(K, n_vision, cfg.sink_index, cfg.block_size)
     active, p_act, pq, bact = ops.q_score(Q, k_lazy, k_act, n_vision, cfg.tau, cfg.preserve_first_head,
                                           cfg.block_size, want_prob=want_prob, O_zero=O_zero)
-    # the compaction only needs K2's flags: it runs beside K3 on the side stream
-    main = torch.cuda.current_stream(Q.device)
-    side = _fork(Q.device)
-    with torch.cuda.stream(side):
-        rows, counts = ops.compact_rows(active, bact, cfg.block_size)
-    for t in (active, bact):
-        t.record_stream(side)
+    rows, counts = ops.compact_rows(active, bact, cfg.block_size)
     if score_source == "probe":
         mass = ops.probe_mass(pq, pk)
         sel = ops.select(mass, K.shape[0], n, cfg.block_size, cfg.p, cfg.granularity)
@@ -128,9 +103,6 @@ def select_device(Q: torch.Tensor, K: torch.Tensor, n_vision: int, cfg: Sparsity
             blk = ops.block_sums(sel.group_scores, cfg.block_size)
             sel.selected, bcounts = ops.top_blocks(blk, n, cfg.block_size, int(sel.info[0]))
             sel.info[4:] = bcounts
-    main.wait_stream(side)  # rows / counts ready for whatever the caller queues next
-    for t in (rows, counts):
-        t.record_stream(main)
     return k_lazy, k_act, pk, active, p_act, pq, rows, counts, mass, sel
 
 
@@ -200,15 +172,8 @@ def sparse_prefill_device(Q: torch.Tensor, K: torch.Tensor, V: torch.Tensor, n_v
     k_lazy, k_act, pk, active, p_act, pq, rows, counts, mass, sel = select_device(Q, K, n_vision, cfg, want_prob, O,
                                                                                   score_source)
     cap = ops.round_up(n, ops.TILE)
-    main = torch.cuda.current_stream(Q.device)
-    side = _fork(Q.device)
-    with torch.cuda.stream(side):  # the two gathers run concurrently
-        V_sel = ops.gather_rows(Vb, sel.selected, sel.counts, cap, ops.TILE)
     K_sel = ops.gather_rows(Kb, sel.selected, sel.counts, cap, ops.TILE)
-    main.wait_stream(side)
-    V_sel.record_stream(main)
-    for t in (Vb, sel.selected, sel.counts):
-        t.record_stream(side)
+    V_sel = ops.gather_rows(Vb, sel.selected, sel.counts, cap, ops.TILE)
     lse = torch.empty(hq, n, device=Q.device, dtype=torch.float32)
     ops.sparse_attn_fwd(Qb, K_sel, V_sel, Vb, rows, counts, sel.selected, sel.counts, cfg.sink_index, O, lse)
     return DevicePrefill(O, lse, active, rows, counts, sel, k_lazy, k_act, pq, pk, mass, K_sel, V_sel, p_act)
