@@ -94,7 +94,8 @@ __device__ unsigned long long g_fwd_trace[8];
 // Profiling build only (VFLAGS=-DOMNI_FWD_CTA_TIMING, profiles/k4_cta_timing.py):
 // per-CTA wall-clock phases of the fast kernel in ns (globaltimer), summed
 // into g_fwd_trace: [0] start -> first QK issued (prologue), [1] tile A's
-// last PV complete -> exit (epilogue), [2] start -> exit, [3] CTAs.
+// last PV complete -> exit (epilogue), [2] start -> exit, [3] CTAs, [4] SM
+// cycles over the CTA (with [2]: the effective SM clock).
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -118,6 +119,7 @@ __device__ __forceinline__ void fwd_tile(int L, bool reuse, const CUtensorMap& t
   extern __shared__ uint8_t smem_raw[];
 #ifdef OMNI_FWD_CTA_TIMING
   const unsigned long long t_start = gtimer();
+  const long long c_start = clock64();
   __shared__ unsigned long long s_t_first, s_t_last;
 #endif
   const int h = L % Hq;
@@ -575,6 +577,7 @@ __device__ __forceinline__ void fwd_tile(int L, bool reuse, const CUtensorMap& t
     atomicAdd(&g_fwd_trace[1], t_end - s_t_last);
     atomicAdd(&g_fwd_trace[2], t_end - t_start);
     atomicAdd(&g_fwd_trace[3], 1ull);
+    atomicAdd(&g_fwd_trace[4], (unsigned long long)(clock64() - c_start));  // SM cycles over the CTA
   }
 #endif
   if (reuse) {  // the next tile re-initialises the barriers

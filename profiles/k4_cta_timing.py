@@ -26,7 +26,10 @@ e.record(); torch.cuda.synchronize()
 lib.omni_debug_fwd_trace(buf)
 ms = s.elapsed_time(e) / k
 ctas = buf[3] / k
+if buf[3] == 0:
+    print(json.dumps({"n": n, "k4_ms": ms, "note": "no fast-kernel CTAs timed"})); sys.exit(0)
 print(json.dumps({"n": n, "k4_ms": ms, "ctas_per_launch": ctas, "prologue_us_per_cta": buf[0] / buf[3] / 1e3,
                   "epilogue_us_per_cta": buf[1] / buf[3] / 1e3, "cta_us": buf[2] / buf[3] / 1e3,
                   "sm_time_used_frac": buf[2] / k / 1e6 / (148 * ms),
-                  "prologue_plus_epilogue_frac_of_sm_time": (buf[0] + buf[1]) / k / 1e6 / (148 * ms)}))
+                  "prologue_plus_epilogue_frac_of_sm_time": (buf[0] + buf[1]) / k / 1e6 / (148 * ms),
+                  "effective_sm_clock_mhz": buf[4] / buf[2] * 1e3}))
