@@ -66,6 +66,19 @@ enum {
 constexpr uint32_t OFF_TMEM = OFF_BAR + 8 * B_COUNT;
 constexpr uint32_t SMEM_BYTES = OFF_TMEM + 16 + 1024;  // + alignment slack
 constexpr uint32_t TMEM_COLS = 512;
+#ifdef OMNI_FWD_WARP_PF
+// Variants build flag: "P ready" as one arrival per softmax warp (after a
+// __syncwarp; the TMEM stores being signalled are complete, tcgen05.wait::st)
+// instead of one per thread.
+constexpr uint32_t PF_COUNT = 2 * BM / 32;
+__device__ __forceinline__ void arrive_pf(uint32_t b) {
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) mbar_arrive(b);
+}
+#else
+constexpr uint32_t PF_COUNT = 2 * BM;
+__device__ __forceinline__ void arrive_pf(uint32_t b) { mbar_arrive(b); }
+#endif
 __device__ __forceinline__ uint32_t col_s(int x) { return 256u * x; }
 __device__ __forceinline__ uint32_t col_o(int x) { return 256u * x + 128u; }
 
@@ -177,7 +190,7 @@ __device__ __forceinline__ void fwd_tile(int L, bool reuse, const CUtensorMap& t
     for (int x = 0; x < 2; ++x) {
       mbar_init(B(B_QF + x), 2 * BM);
       mbar_init(B(B_SF + x), 1);
-      mbar_init(B(B_PF + x), 2 * BM);
+      mbar_init(B(B_PF + x), PF_COUNT);
       mbar_init(B(B_PV + x), 1);
     }
     for (int s = 0; s < NST; ++s) {
@@ -329,7 +342,7 @@ __device__ __forceinline__ void fwd_tile(int L, bool reuse, const CUtensorMap& t
         tick(0);
         if constexpr (POLY < 0) {  // profiling only: the MMA / TMA pipeline without softmax work
           tc_fence_before();
-          mbar_arrive(B(B_PF + x));
+          arrive_pf(B(B_PF + x));
           l_run = 1.f;
           continue;
         }
@@ -439,7 +452,7 @@ __device__ __forceinline__ void fwd_tile(int L, bool reuse, const CUtensorMap& t
             const float rs = chunk_fast(0, m_run) + chunk_fast(1, m_run);
             tmem_wait_st();
             tc_fence_before();
-            mbar_arrive(B(B_PF + x));
+            arrive_pf(B(B_PF + x));
             // rows that have seen no visible key yet (m_run = -inf; their
             // masked P are NaN and never used) are excluded from both tests
             if (m_run != -INFINITY && !(rs <= 0x1p64f)) atomicExch(status, 1);  // some P may exceed 2^64
@@ -512,7 +525,7 @@ __device__ __forceinline__ void fwd_tile(int L, bool reuse, const CUtensorMap& t
         tick(3);
         tmem_wait_st();
         tc_fence_before();
-        mbar_arrive(B(B_PF + x));
+        arrive_pf(B(B_PF + x));
       }
       tick(4);
       if constexpr (TRACE) {
@@ -977,6 +990,18 @@ int omni_sparse_attn_fwd_pair(const void* Q, const void* K_sel, const void* V_se
                               const int32_t* counts, const int32_t* selected, const int32_t* sel_counts,
                               int n_q_heads, int n_kv_heads, int seq_len, int cap, int sink_index, void* O,
                               float* lse, int poly, cudaStream_t stream);
+int omni_sparse_attn_fwd_pp(const void* Q, const void* K_sel, const void* V_sel, const void* V, const int32_t* rows,
+                            const int32_t* counts, const int32_t* selected, const int32_t* sel_counts, int n_q_heads,
+                            int n_kv_heads, int seq_len, int cap, int sink_index, void* O, float* lse, int32_t* status,
+                            int poly, cudaStream_t stream);
+int omni_sparse_attn_fwd_sp(const void* Q, const void* K_sel, const void* V_sel, const void* V, const int32_t* rows,
+                            const int32_t* counts, const int32_t* selected, const int32_t* sel_counts, int n_q_heads,
+                            int n_kv_heads, int seq_len, int cap, int sink_index, void* O, float* lse, int32_t* status,
+                            int poly, cudaStream_t stream);
+int omni_sparse_attn_fwd_db(const void* Q, const void* K_sel, const void* V_sel, const void* V, const int32_t* rows,
+                            const int32_t* counts, const int32_t* selected, const int32_t* sel_counts, int n_q_heads,
+                            int n_kv_heads, int seq_len, int cap, int sink_index, void* O, float* lse, int32_t* status,
+                            int poly, cudaStream_t stream);
 #endif
 
 // status: device int workspace (nullable). With it the FAST kernel runs first
@@ -1035,6 +1060,41 @@ extern "C" int omni_sparse_attn_fwd_ex(const void* Q, const void* K_sel, const v
         tk, tv, static_cast<const __nv_bfloat16*>(Q), static_cast<const __nv_bfloat16*>(V), rows, counts, selected,
         sel_counts, n_q_heads, rep, seq_len, cap, seq_len, sink_index, n_tiles, static_cast<__nv_bfloat16*>(O), lse,
         nullptr, status);
+    return omni_launch_check();
+  }
+  // 1: CTA-pair ping-pong (attn_fwd_pp.cu), 2: double-buffered S (attn_fwd_db.cu),
+  // 3: shared S / separate P (attn_fwd_sp.cu)
+  static const int alt_impl = [] {
+    const char* e = getenv("OMNI_FWD_IMPL");
+    return !e ? 0 : strcmp(e, "pp") == 0 ? 1 : strcmp(e, "db") == 0 ? 2 : strcmp(e, "sp") == 0 ? 3 : 0;
+  }();
+  if (alt_impl) {
+    static const bool pp_fast = [] {
+      const char* e = getenv("OMNI_FWD_FAST");
+      return !(e && atoi(e) == 0);
+    }();
+    int32_t* pst = (pp_fast && poly_env >= 0) ? status : nullptr;
+    if (pst) OMNI_CUDA_TRY(cudaMemsetAsync(pst, 0, sizeof(int32_t), st_));
+    int st = (alt_impl == 1 ? omni_sparse_attn_fwd_pp : alt_impl == 2 ? omni_sparse_attn_fwd_db : omni_sparse_attn_fwd_sp)(
+        Q, K_sel, V_sel, V, rows, counts, selected, sel_counts, n_q_heads, n_kv_heads, seq_len, cap, sink_index, O,
+        lse, pst, poly_env, st_);
+    if (st || !pst) return st;
+    // the single-CTA safe kernel redoes the launch if a tile's logits jumped beyond 2^64
+    CUtensorMap tk, tv;
+    st = omni_make_tmap_rows(&tk, K_sel, (uint64_t)n_kv_heads * cap, 128, 2, 64, fwd::BN);
+    if (st) return st;
+    st = omni_make_tmap_rows(&tv, V_sel, (uint64_t)n_kv_heads * cap, 128, 2, 64, fwd::BN);
+    if (st) return st;
+    auto redo = fwd::sparse_fwd_kernel<kDefaultPoly, false, false, true>;
+    OMNI_CUDA_TRY(omni_smem_attr(redo, (int)fwd::SMEM_BYTES));
+    const int n_tiles = (seq_len + 2 * fwd::BM - 1) / (2 * fwd::BM);
+    int dev = 0, sms = 148;
+    OMNI_CUDA_TRY(cudaGetDevice(&dev));
+    OMNI_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    redo<<<std::min<unsigned>(n_tiles * n_q_heads, (unsigned)sms), fwd::NTHREADS, fwd::SMEM_BYTES, st_>>>(
+        tk, tv, static_cast<const __nv_bfloat16*>(Q), static_cast<const __nv_bfloat16*>(V), rows, counts, selected,
+        sel_counts, n_q_heads, n_q_heads / n_kv_heads, seq_len, cap, seq_len, sink_index, n_tiles,
+        static_cast<__nv_bfloat16*>(O), lse, nullptr, pst);
     return omni_launch_check();
   }
   if (!single)

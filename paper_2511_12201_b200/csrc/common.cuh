@@ -388,6 +388,18 @@ __device__ __forceinline__ void umma_pair_ts_ws(uint32_t d_tmem, uint32_t a_tmem
       "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// Pair MMA with both operands in shared memory: A = this CTA's 128 rows in
+// each CTA (same offset), B split along N between the CTAs.
+__device__ __forceinline__ void umma_pair_ss_ws(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                                uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t.reg .b32 rx;\n\t"
+      "elect.sync rx|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
 // Commit of the leader's pair MMAs, arriving on the mbarrier at the same
 // offset in both CTAs of the pair.
 __device__ __forceinline__ void umma_commit_pair_ws(uint32_t bar) {

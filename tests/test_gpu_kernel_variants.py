@@ -1,6 +1,7 @@
 """K4 kernel variants (the OMNI_VARIANTS build, libomnisparse_variants.so,
 selected once per process by environment variables) against the oracle: the single-CTA ping-pong kernel at several MUFU / FMA-pipe
-exp2 splits and the CTA-pair (cta_group::2) kernel. Each variant runs in its
+exp2 splits, the CTA-pair (cta_group::2) kernel, the row-per-thread kernel
+the CTA-pair ping-pong kernel and the double-buffered-S kernel. Each variant runs in its
 own subprocess on a GQA workload with ragged N (partial tiles, staircase)."""
 
 import json
@@ -75,10 +76,20 @@ for _g in range(K.shape[0]):
                                                  ("single", "6", "1", "ramp"), ("single", "6", "0", "ramp"),
                                                  ("pair", "0", "1", False), ("pair", "4", "1", False),
                                                  ("rpt", "6", "1", False), ("rpt", "6", "1", True),
-                                                 ("rpt", "6", "1", "ramp")])
+                                                 ("rpt", "6", "1", "ramp"),
+                                                 ("pp", "6", "1", False), ("pp", "6", "1", True),
+                                                 ("pp", "6", "1", "ramp"), ("pp", "6", "0", False),
+                                                 ("pp", "6", "0", "ramp"),
+                                                 ("db", "6", "1", False), ("db", "6", "1", True),
+                                                 ("db", "6", "1", "ramp"), ("db", "6", "0", False),
+                                                 ("db", "6", "0", "ramp"), ("db", "0", "1", False),
+                                                 ("sp", "6", "1", False), ("sp", "6", "1", True),
+                                                 ("sp", "6", "1", "ramp"), ("sp", "6", "0", False),
+                                                 ("sp", "6", "0", "ramp"), ("sp", "6", "0", True)])
 def test_forward_variant_matches_oracle(impl, poly, fast, jump):
     env = dict(os.environ, OMNI_FWD_IMPL=impl, OMNI_FWD_POLY=poly, OMNI_FWD_FAST=fast,
-               OMNI_LIBRARY=os.path.join(ROOT, "paper_2511_12201_b200", "lib", "libomnisparse_variants.so"))
+               OMNI_LIBRARY=os.environ.get("OMNI_VARIANTS_LIBRARY",
+                                           os.path.join(ROOT, "paper_2511_12201_b200", "lib", "libomnisparse_variants.so")))
     snippet = RAMP if jump == "ramp" else JUMP if jump else ""
     code = CODE.replace("Q, K, V = round_bf16(Q), round_bf16(K), round_bf16(V)",
                         snippet + "Q, K, V = round_bf16(Q), round_bf16(K), round_bf16(V)")
@@ -87,6 +98,6 @@ def test_forward_variant_matches_oracle(impl, poly, fast, jump):
     r = json.loads(out.stdout.strip().splitlines()[-1])
     assert not r["nan"]
     assert r["scaled_err"] <= 1.0, r  # |err| <= 0.02 + 0.02 |ref| (bf16 P, fp32 accumulation)
-    if impl in ("single", "rpt") and fast == "1":
+    if impl in ("single", "rpt", "pp", "db", "sp") and fast == "1":
         # the fast kernel hands over to the safe re-run exactly when a logit jump exceeds 2^64
         assert r["fallback"] == (1 if jump is True else 0), r
