@@ -108,7 +108,9 @@ __device__ unsigned long long g_fwd_trace[8];
 // per-CTA wall-clock phases of the fast kernel in ns (globaltimer), summed
 // into g_fwd_trace: [0] start -> first QK issued (prologue), [1] tile A's
 // last PV complete -> exit (epilogue), [2] start -> exit, [3] CTAs, [4] SM
-// cycles over the CTA (with [2]: the effective SM clock).
+// cycles over the CTA (with [2]: the effective SM clock), [5] start -> set-up
+// barrier, [6] start -> thread 64's row / Q loads done, [7] start -> its
+// visible-key count done.
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -133,7 +135,7 @@ __device__ __forceinline__ void fwd_tile(int L, bool reuse, const CUtensorMap& t
 #ifdef OMNI_FWD_CTA_TIMING
   const unsigned long long t_start = gtimer();
   const long long c_start = clock64();
-  __shared__ unsigned long long s_t_first, s_t_last;
+  __shared__ unsigned long long s_t_first, s_t_last, s_t_vis;
 #endif
   const int h = L % Hq;
   // Heaviest (latest rows) tile pairs first, counted down from the largest
@@ -179,7 +181,21 @@ __device__ __forceinline__ void fwd_tile(int L, bool reuse, const CUtensorMap& t
 #pragma unroll
     for (int c = 0; c < 8; ++c) qv[c] = rvalid ? __ldg(qrow + c) : make_uint4(0, 0, 0, 0);
   }
-  const int vis = rvalid ? count_le(selg, nsel, pos) : 0;
+#ifdef OMNI_FWD_CTA_TIMING
+  const unsigned long long t_loaded = gtimer();  // row position and Q half-row loaded
+#endif
+  // visible-key counts: a warp's 32 rows are consecutive compacted rows, so
+  // one warp-cooperative search (32 pivots per level, then a scan of the
+  // window between its smallest and largest row) replaces 32 binary searches
+  // of ~15 dependent L2 loads each (6.8 of the 10.7 us CTA prologue at 64K)
+  int vis = warp >= 2 ? count_le_warp(selg, nsel, pos, rvalid) : 0;
+  if (!rvalid) vis = 0;
+#ifdef OMNI_FWD_CTA_TIMING
+  if (FAST && threadIdx.x == 64) {
+    s_t_vis = gtimer();
+    atomicAdd(&g_fwd_trace[6], t_loaded - t_start);
+  }
+#endif
   if (warp >= 2 && hf == 0) {
     if (is == nrows_s - 1) s_nt[xs] = (vis + BN - 1) / BN;
     if (nrows_s <= 0 && is == 0) s_nt[xs] = 0;
@@ -208,6 +224,9 @@ __device__ __forceinline__ void fwd_tile(int L, bool reuse, const CUtensorMap& t
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+#ifdef OMNI_FWD_CTA_TIMING
+  if (FAST && threadIdx.x == 0) atomicAdd(&g_fwd_trace[5], gtimer() - t_start);  // start -> set-up barrier
+#endif
   const uint32_t tmem = *tmem_slot;
   const int ntA = s_nt[0], ntB = s_nt[1];
   const int ntm = max(ntA, ntB);
@@ -591,6 +610,7 @@ __device__ __forceinline__ void fwd_tile(int L, bool reuse, const CUtensorMap& t
     atomicAdd(&g_fwd_trace[2], t_end - t_start);
     atomicAdd(&g_fwd_trace[3], 1ull);
     atomicAdd(&g_fwd_trace[4], (unsigned long long)(clock64() - c_start));  // SM cycles over the CTA
+    atomicAdd(&g_fwd_trace[7], s_t_vis - t_start);  // start -> thread 64's visible-key count
   }
 #endif
   if (reuse) {  // the next tile re-initialises the barriers
@@ -684,7 +704,8 @@ __device__ __forceinline__ void fwd_tile_rpt(int L, const CUtensorMap& tm_k, con
 #pragma unroll
     for (int c = 0; c < 16; ++c) qv[c] = rvalid ? __ldg(qrow + c) : make_uint4(0, 0, 0, 0);
   }
-  const int vis = rvalid ? count_le(selg, nsel, pos) : 0;
+  int vis = warp >= 2 ? count_le_warp(selg, nsel, pos, rvalid) : 0;
+  if (!rvalid) vis = 0;
   if (warp >= 2) {
     if (is == nrows_s - 1) s_nt[xs] = (vis + BN - 1) / BN;
     if (nrows_s <= 0 && is == 0) s_nt[xs] = 0;

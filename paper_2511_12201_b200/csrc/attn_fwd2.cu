@@ -128,7 +128,8 @@ sparse_fwd_pair_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_co
 #pragma unroll
     for (int c = 0; c < 4; ++c) qv[c] = rvalid ? __ldg(qrow + c) : make_uint4(0, 0, 0, 0);
   }
-  const int vis = rvalid ? count_le(selg, nsel, pos) : 0;
+  int vis = warp >= 2 ? count_le_warp(selg, nsel, pos, rvalid) : 0;
+  if (!rvalid) vis = 0;
   if (warp >= 2 && cc == 0) {
     if (i == nrows - 1) *s_nt = (vis + BN - 1) / BN;
     if (nrows <= 0 && i == 0) *s_nt = 0;

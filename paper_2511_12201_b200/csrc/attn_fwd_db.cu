@@ -116,7 +116,8 @@ sparse_fwd_db_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_cons
 #pragma unroll
     for (int c = 0; c < 16; ++c) qv[c] = rvalid ? __ldg(qrow + c) : make_uint4(0, 0, 0, 0);
   }
-  const int vis = rvalid ? count_le(selg, nsel, pos) : 0;
+  int vis = warp >= 2 ? count_le_warp(selg, nsel, pos, rvalid) : 0;
+  if (!rvalid) vis = 0;
   if (warp >= 2) {
     if (is == nrows_s - 1) s_nt[xs] = (vis + BK - 1) / BK;
     if (nrows_s <= 0 && is == 0) s_nt[xs] = 0;

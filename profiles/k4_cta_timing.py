@@ -32,4 +32,6 @@ print(json.dumps({"n": n, "k4_ms": ms, "ctas_per_launch": ctas, "prologue_us_per
                   "epilogue_us_per_cta": buf[1] / buf[3] / 1e3, "cta_us": buf[2] / buf[3] / 1e3,
                   "sm_time_used_frac": buf[2] / k / 1e6 / (148 * ms),
                   "prologue_plus_epilogue_frac_of_sm_time": (buf[0] + buf[1]) / k / 1e6 / (148 * ms),
-                  "effective_sm_clock_mhz": buf[4] / buf[2] * 1e3}))
+                  "effective_sm_clock_mhz": buf[4] / buf[2] * 1e3,
+                  "start_to_loads_us": buf[6] / buf[3] / 1e3, "start_to_vis_us": buf[7] / buf[3] / 1e3,
+                  "start_to_setup_barrier_us": buf[5] / buf[3] / 1e3}))
