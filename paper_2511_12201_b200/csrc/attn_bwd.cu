@@ -725,18 +725,20 @@ dkv2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
   __shared__ int s_first, s_total;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int h = g * rep + rs;
-  if (threadIdx.x == 0) {
+  if (warp == 0) {
+    // first compact row whose position >= first_key (it sees key k0): the
+    // rows below it, by a warp-cooperative search (32 pivots per level; a
+    // per-thread binary search is ~14 dependent L2 loads, ~0.5 us each while
+    // the other SMs stream)
     const int first_key = __ldg(sel + (size_t)g * N + k0);
     const int cnt = __ldg(counts + h);
-    // first compact row whose position >= first_key (it sees key k0)
-    const int32_t* rh = rows + (size_t)h * N;
-    int lo = 0, hi = cnt;
-    while (lo < hi) {
-      const int mid = (lo + hi) >> 1;
-      if (__ldg(rh + mid) < first_key) lo = mid + 1; else hi = mid;
+    const int lo = count_le_warp(rows + (size_t)h * N, cnt, first_key - 1, true);
+    if (lane == 0) {
+      s_first = lo / BR;
+      s_total = max(0, (cnt + BR - 1) / BR - lo / BR);
     }
-    s_first = lo / BR;
-    s_total = max(0, (cnt + BR - 1) / BR - lo / BR);
+  }
+  if (threadIdx.x == 0) {
     tma_prefetch_desc(&tm_q);
     tma_prefetch_desc(&tm_do);
     tma_prefetch_desc(&tm_k);
