@@ -7,3 +7,6 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smok
 timeout 400 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc $?"
 timeout 400 python bench.py --impl reference > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo "ref rc $?"
 bash profiles/r02_hbm_profile.sh
+# K4 (the dominant kernel) at HEAD: one full ncu capture of the fast kernel (3rd launch)
+ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:"sparse_fwd_kernel" -s 2 -c 1 \
+    -o gpurun_out/r02_k4 -f python profiles/ncu_k4_driver.py > gpurun_out/r02_k4.log 2>&1; echo "ncu k4 rc $?"
