@@ -8,10 +8,10 @@
 // bulk-copy ring of probe blocks; the generic kernels (one CTA per (probe
 // block, head)) serve other dtypes, head sizes, the want_prob path and the
 // A/B switch OMNI_QSCORE_F64. Measured at 64K tokens (28 / 4 heads, one
-// B200, profiles/r02_notes.md): K1 0.024 ms (2.8 TB/s), K2 0.177 ms (3.9
-// TB/s, 0.60 of the measured copy bandwidth; the float64 column sums of the
-// pooled queries keep it issue-bound) vs 0.028 / 0.194 ms for the generic
-// kernels.
+// B200, device time in a CUDA graph, profiles/r02_notes.md): K1 0.016 ms
+// (with probe_finish; 4.2 TB/s, 0.65 of the measured copy bandwidth), K2
+// 0.172 ms (4.05 TB/s, 0.62; the float64 column sums of the pooled queries
+// keep it issue-bound) vs 0.028 / 0.194 ms (eager) for the generic kernels.
 #include "common.cuh"
 
 namespace omni {
