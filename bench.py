@@ -627,16 +627,17 @@ def run_ours(args):
         achieved = flops / (fa_ms / 1e3) / 1e12
         traffic = None
         try:  # dram bytes per K4 launch from the committed ncu capture of the same workload
-            with open(os.path.join(ROOT, "profiles", "r01_k4_traffic.json")) as f:
+            with open(os.path.join(ROOT, "profiles", "r02_k4_traffic.json")) as f:
                 traffic = json.load(f)["dram_bytes_per_launch"]
         except Exception:  # noqa: BLE001
             pass
         line["roofline"] = {"bound": "tensor", "kernel": "omni sparse_fwd_kernel (K4)", "achieved": achieved,
                             "peak": tc_peak, "unit": "TFLOP/s", "frac": achieved / tc_peak, "traffic": traffic,
                             "traffic_note": "dram__bytes_read.sum + dram__bytes_write.sum per launch "
-                                            "(profiles/r01_k4_traffic.json); K4 is tensor-bound, its DRAM traffic "
-                                            "(Q rows, K/V tiles re-read past L2, O rows) is ~1.1 GB per 9.6 ms",
+                                            "(profiles/r02_k4_traffic.json); K4 is tensor-bound, its DRAM traffic "
+                                            "(Q rows, K/V tiles re-read past L2, O rows) is ~1.16 GB per ~9 ms",
                             "peak_source": f"{peak_src} bf16 burst (MEASURED_PEAKS.json)",
+                            "peak_sustained": tc_sus, "frac_of_sustained": achieved / tc_sus,
                             "algorithmic_flops_per_launch": flops, "launch_ms": fa_ms}
         # parity: this run's decision margins + the committed oracle report
         st = res.selection.stats.cpu().tolist()
