@@ -447,7 +447,6 @@ def train_section(args, steps, warmup, tc_peak):
     dO = torch.randn_like(Q)
 
     def sparse_step():  # = autograd.sparse_attention (the public API), keeping the plan for the FLOP count
-        Q.grad = K.grad = V.grad = None  # a training loop's zero_grad(set_to_none=True); the dense step does the same
         out = torch.empty(Q.shape, device=Q.device, dtype=torch.bfloat16)
         with torch.no_grad():
             _, _, _, _, _, _, rows, counts, _, sel = select_device(Q.detach(), K.detach(), nv, cfg, O_zero=out)
@@ -459,8 +458,8 @@ def train_section(args, steps, warmup, tc_peak):
     ms = time_cuda(sparse_step, steps, warmup)
     res = {"workload": f"sparse attention fwd+bwd, {HQ}/{HKV} heads, d={D}, {n} tokens (C4)", "ms_per_step": ms,
            "tok_s": n / (ms / 1e3),
-           "step": "selection (no_grad) + forward + backward to Q/K/V grads, grads set to None before each step in "
-                   "both arms (zero_grad(set_to_none=True))"}
+           "step": "selection (no_grad) + forward + backward, gradients accumulated into the leaves' .grad in "
+                   "both arms"}
     # K5 roofline: backward FLOPs = 2.5 x the forward's algorithmic FLOPs
     # (dq: 3 GEMMs, dkv: 4 GEMMs per visible tile pair vs the forward's 2),
     # counted from this step's index sets; K5 = bwd_prep + dq + dkv, timed
@@ -508,7 +507,6 @@ def train_section(args, steps, warmup, tc_peak):
         g4 = dO.unsqueeze(0)
 
         def dense_step():
-            q4.grad = k4.grad = v4.grad = None
             with sdpa_kernel(SDPBackend.CUDNN_ATTENTION):
                 o = torch.nn.functional.scaled_dot_product_attention(q4, k4, v4, is_causal=True, enable_gqa=True)
             o.backward(g4)
@@ -938,7 +936,6 @@ def multi_rank_decode_train(args, line, world, rank, hbm_peak, plan):
         del Q, K, V
 
         def train_step():
-            Ql.grad = Kl.grad = Vl.grad = None  # zero_grad(set_to_none=True), as the 1-GPU step
             O = sparse_attention_sharded(Ql, Kl, Vl, plan, nv, world, cfg, kv_group=kvg)
             O.backward(dO)
 
